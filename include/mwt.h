@@ -1,0 +1,180 @@
+/*
+ * mwt.h -- C ABI of the B200 batched 2D ray-query engine (libmwt.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `mintri`
+ * (arXiv 2112.05570): stackless closest-hit traversal of rays through a
+ * constrained triangulation, plus the point location that seeds it and the
+ * like-for-like roped kd-tree / SAH BVH engines.  The reference exposes this
+ * path only as Python functions (it has no native layer); each entry point
+ * below names the reference function it replaces.  A ctypes binding of every
+ * symbol lives in paper_2112_05570_b200/_lib.py, and INTEGRATION.md shows the
+ * shim a `mintri` maintainer would add.
+ *
+ * Conventions
+ *  - Plain pointers and sizes; no torch / CUDA types in the signatures.
+ *    `stream` is a cudaStream_t passed as void* (NULL = legacy default).
+ *  - Functions named *_dev take DEVICE pointers and are asynchronous on
+ *    `stream`; functions named *_host take HOST pointers, copy in and out and
+ *    synchronise before returning.
+ *  - Rays are float64 quadruples (ox, oy, dx, dy), row-major, 32 B per ray.
+ *    Directions are used exactly as given (the reference's `Ray` has already
+ *    renormalised them, geometry.py:68-74).
+ *  - Every function returns 0 on success or a negative MWT_E* code; the
+ *    message of the last failure on the calling thread is mwt_last_error().
+ *  - Per-ray results: seg (int32, -1 = no hit), t and u (float64, NaN on a
+ *    miss), steps (int32), status (uint32 bit set, MWT_ST_*).
+ */
+#ifndef MWT_H
+#define MWT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MWT_ABI_VERSION 1
+
+/* return codes */
+#define MWT_OK 0
+#define MWT_E_INVALID (-1)   /* bad argument / malformed mesh */
+#define MWT_E_CUDA (-2)      /* CUDA runtime failure */
+#define MWT_E_NOMEM (-3)
+#define MWT_E_TOPOLOGY (-4)  /* neighbour symmetry broken (trimesh.py:283-311) */
+
+/* per-ray status bits (degeneracy enumeration) */
+#define MWT_ST_ERROR 1u        /* TraversalError: loop or no exit (accel.py:164-191) */
+#define MWT_ST_FALLBACK 2u     /* no candidate exit edge, fallback used (accel.py:188-189) */
+#define MWT_ST_GRAZING 4u      /* ray_segment_intersect None at a constrained edge (accel.py:199-207) */
+#define MWT_ST_CANON 8u        /* canonical() moved the hit to a lower id (accel.py:82-98) */
+#define MWT_ST_PARALLEL 16u    /* parallel branch of ray_segment_intersect (geometry.py:149-161) */
+#define MWT_ST_ZERO_SIDE 32u   /* exact-zero side value at an exit candidate */
+#define MWT_ST_MULTI 64u       /* more than one exit candidate in one triangle */
+#define MWT_ST_LOC_TIE 128u    /* locate flood visited >1 containing triangle (accel.py:226-238) */
+#define MWT_ST_LOC_BRUTE 256u  /* anchor walk failed, brute-force scan (accel.py:287-288) */
+#define MWT_ST_LOC_OUTSIDE 512u /* point outside every triangle: nearest centroid (accel.py:245-246) */
+#define MWT_ST_OVERFLOW 1024u  /* device capacity exceeded (flood/stack); result invalid */
+
+/* ray generator modes (engine-defined) */
+#define MWT_RAYS_BOX_ENTRY 0   /* isotropic lines through the box, origin at box entry */
+#define MWT_RAYS_INTERIOR 1    /* origin uniform in the box, isotropic direction */
+
+/* histogram layout written by mwt_trace_generated_dev / mwt_histogram_dev */
+#define MWT_HIST_STEP_BINS 1024 /* bins 0..1022 exact step counts, 1023 = overflow */
+#define MWT_HIST_HIT 1024       /* rays with a hit */
+#define MWT_HIST_MISS 1025      /* rays without a hit (boundary / open edge) */
+#define MWT_HIST_STEPS_SUM 1026 /* sum of tri_steps */
+#define MWT_HIST_STATUS0 1027   /* 11 counters, one per MWT_ST_* bit */
+#define MWT_HIST_LEN 1040       /* int64 entries */
+
+typedef struct mwt_mesh mwt_mesh;
+typedef struct mwt_bvh mwt_bvh;
+typedef struct mwt_kd mwt_kd;
+
+typedef struct {
+    int32_t num_vertices, num_triangles, num_segments;
+    int32_t anchor_res;            /* TriLocator grid resolution (accel.py:265-266) */
+    int32_t anchors_not_strict;    /* anchor centres on an edge/vertex (order-dependent seeds) */
+    int32_t device;
+    int64_t device_bytes;          /* total device footprint of the packed mesh */
+    int64_t walk_record_bytes;     /* bytes per triangle read by one walk step */
+} mwt_mesh_info;
+
+/* Library / error plumbing */
+int mwt_abi_version(void);
+const char *mwt_last_error(void);
+int mwt_device_count(int *count);
+
+/* K1 -- mesh packer.
+ * Replaces: building `Triangulation` + `SceneIndex` for the walk
+ *   (trimesh.py:93-150 data model; accel.py:64-80 SceneIndex; accel.py:263-282 anchors).
+ * Inputs are the reference data model exactly as `load_triangulation`
+ * (trimesh.py:1309-1337) / `parse_scene` (scene.py:135-165) hold it:
+ *   vx, vy[nverts]; tri_v, tri_nbr, tri_flag[3*ntris] (nbr -1 = None,
+ *   flag -1 = INTERNAL or a scene segment id); seg_xy[4*nsegs] (ax, ay, bx, by);
+ *   seg_kind[nsegs] (0 = GEOMETRY 'G', 1 = BOUNDARY 'B').
+ * Host arrays are copied; the handle owns the device copies. */
+int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts,
+                    const int32_t *tri_v, const int32_t *tri_nbr, const int32_t *tri_flag,
+                    int32_t ntris, const double *seg_xy, const uint8_t *seg_kind, int32_t nsegs,
+                    int device, mwt_mesh **out);
+int mwt_mesh_destroy(mwt_mesh *mesh);
+int mwt_mesh_info_get(const mwt_mesh *mesh, mwt_mesh_info *out);
+/* copy the device-side anchor table (res*res int32) to host, for tests */
+int mwt_mesh_anchors(const mwt_mesh *mesh, int32_t *out_host);
+
+/* K2 -- seeded ray generator.  No reference counterpart (the reference's
+ * sample_rays, experiment.py:29-63, draws interior origins); realises the
+ * BASELINE.json ray recipe.  box = (x0, y0, x1, y1); rays for global indices
+ * first .. first+n-1 go to rays_out (device, 4*n doubles). */
+int mwt_raygen_dev(int mode, const double *box, uint64_t seed, uint64_t first, int64_t n,
+                   double *rays_out, void *stream);
+
+/* K3 -- start-triangle location.
+ * Replaces: TriLocator(tri).locate(p) / locate_triangle(tri, p, "anchor")
+ *   (accel.py:284-289, :333-353).  pts = n (x, y) pairs (device). */
+int mwt_locate_dev(const mwt_mesh *mesh, const double *pts, int64_t n, int32_t *out_tid,
+                   uint32_t *out_status, void *stream);
+
+/* K4 -- the MWT walk.
+ * Replaces: traverse_triangulation(tri, ray, start_tri, index) (accel.py:138-213),
+ *   with start_tri = TriLocator.locate(origin) when start == NULL
+ *   (the per-ray loop of run_experiment, experiment.py:166-171).
+ * Any output pointer may be NULL (not written).  out_start receives the
+ * start triangle actually used. */
+int mwt_trace_dev(const mwt_mesh *mesh, const double *rays, const int32_t *start, int64_t n,
+                  int32_t *out_start, int32_t *out_seg, double *out_t, double *out_u,
+                  int32_t *out_steps, uint32_t *out_status, void *stream);
+/* Same as mwt_trace_dev on HOST buffers (copies in, traces, copies out, syncs). */
+int mwt_trace_host(const mwt_mesh *mesh, const double *rays, const int32_t *start, int64_t n,
+                   int32_t *out_start, int32_t *out_seg, double *out_t, double *out_u,
+                   int32_t *out_steps, uint32_t *out_status);
+
+/* K2+K3+K4+K7 fused: generate rays first..first+n-1 on device, locate, walk,
+ * write optional per-ray outputs and ADD into hist (device int64[MWT_HIST_LEN],
+ * may be NULL).  This is the benchmark kernel; rays never touch HBM. */
+int mwt_trace_generated_dev(const mwt_mesh *mesh, int mode, const double *box, uint64_t seed,
+                            uint64_t first, int64_t n, int32_t *out_seg, double *out_t,
+                            int32_t *out_steps, int64_t *hist, void *stream);
+
+/* K7 -- accumulate per-ray results into a histogram (device). */
+int mwt_histogram_dev(const int32_t *seg, const int32_t *steps, const uint32_t *status, int64_t n,
+                      int64_t *hist, void *stream);
+
+/* K5 -- SAH BVH walk.
+ * Replaces: bvh_intersect(bvh, ray) / Bvh.intersect (accel.py:482-518, :428).
+ * The tree is the reference Bvh flattened in DFS preorder (node 0 = root):
+ * box[4*nnodes]; left/right child index or -1 for a leaf; leaf prims
+ * prims[prim_off .. prim_off+prim_cnt) in reference order. */
+int mwt_bvh_create(const mwt_mesh *mesh, int32_t nnodes, const double *box, const int32_t *left,
+                   const int32_t *right, const int32_t *prim_off, const int32_t *prim_cnt,
+                   int32_t nprims, const int32_t *prims, mwt_bvh **out);
+int mwt_bvh_destroy(mwt_bvh *bvh);
+int mwt_bvh_trace_dev(const mwt_bvh *bvh, const double *rays, int64_t n, int32_t *out_seg,
+                      double *out_t, double *out_u, int32_t *out_node_tests,
+                      int32_t *out_prim_tests, uint32_t *out_status, void *stream);
+
+/* K6 -- roped kd-tree walk.
+ * Replaces: kd_intersect(kd, ray) / RopedKdTree.intersect (accel.py:761-832, :726),
+ * start leaf by RopedKdTree.locate_leaf(origin, direction) (accel.py:712-724).
+ * Node table in DFS preorder: axis (-1 = leaf), pos, left, right, box[4],
+ * ropes[4] (node index or -1), rope_cost[4] = max(1, ceil(log2(count))),
+ * leaf prims as for the BVH; num_leaves sets the walk guard 4*leaves+16. */
+int mwt_kd_create(const mwt_mesh *mesh, int32_t nnodes, int32_t num_leaves, const int32_t *axis,
+                  const double *pos, const int32_t *left, const int32_t *right, const double *box,
+                  const int32_t *ropes, const int32_t *rope_cost, const int32_t *prim_off,
+                  const int32_t *prim_cnt, int32_t nprims, const int32_t *prims, mwt_kd **out);
+int mwt_kd_destroy(mwt_kd *kd);
+int mwt_kd_trace_dev(const mwt_kd *kd, const double *rays, int64_t n, int32_t *out_seg,
+                     double *out_t, double *out_u, int32_t *out_nodes, int32_t *out_rope_steps,
+                     int32_t *out_prim_tests, uint32_t *out_status, void *stream);
+
+/* Brute-force closest hit (the reference's oracle engine).
+ * Replaces: brute_force_closest(scene, ray, index) (accel.py:101-132). */
+int mwt_brute_force_dev(const mwt_mesh *mesh, const double *rays, int64_t n, int32_t *out_seg,
+                        double *out_t, double *out_u, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MWT_H */

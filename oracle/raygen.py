@@ -1,0 +1,98 @@
+"""numpy host twin of the engine's seeded ray generator.
+
+TEST INFRASTRUCTURE ONLY (see oracle/mwt_oracle.c header).  Bit-identical to
+``orc_raygen`` (oracle/mwt_oracle.c) and to the device generator in
+``paper_2112_05570_b200/csrc/mwt_kernels.cu``: counter-based SplitMix64 draws
+keyed by (seed, stream, ray index), doubles from the top 53 bits, isotropic
+directions by unit-disk rejection + IEEE sqrt and division (no cos/sin), and
+only + - * / sqrt afterwards (numpy never fuses a*b+c).
+
+The reference has no box-entry generator; its ``sample_rays``
+(experiment.py:29-63) draws interior origins with PCG64 and cos/sin.  This
+generator realises BASELINE.json's ray recipe: theta ~ U[0, 2pi), offset
+uniform over the box's projected width, origin at the box entry point.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+GOLDEN = np.uint64(0x9E3779B97F4A7C15)
+C1 = np.uint64(0xBF58476D1CE4E5B9)
+C2 = np.uint64(0x94D049BB133111EB)
+STREAM_MUL = np.uint64(0xD1B54A32D192ED03)
+
+MODE_BOX_ENTRY = 0
+MODE_INTERIOR = 1
+
+
+def _mix(z):
+    with np.errstate(over="ignore"):
+        z = (z ^ (z >> np.uint64(30))) * C1
+        z = (z ^ (z >> np.uint64(27))) * C2
+        return z ^ (z >> np.uint64(31))
+
+
+def ray_key(seed: int, stream: int) -> np.uint64:
+    with np.errstate(over="ignore"):
+        a = _mix(np.uint64(seed) + GOLDEN)
+        return _mix(a ^ (np.uint64(stream) * STREAM_MUL))
+
+
+def _u01(s0, k: int):
+    with np.errstate(over="ignore"):
+        z = _mix(s0 + np.uint64(k + 1) * GOLDEN)
+    return (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
+
+
+def _clamp(v, lo, hi):
+    # C's ``v < lo ? lo : (v > hi ? hi : v)`` (keeps the sign of a zero)
+    return np.where(v < lo, lo, np.where(v > hi, hi, v))
+
+
+def raygen(mode: int, box, seed: int, first: int, n: int) -> np.ndarray:
+    """(n, 4) float64 array of rays (ox, oy, dx, dy)."""
+    key = ray_key(seed, mode)
+    idx = np.arange(first, first + n, dtype=np.uint64)
+    s0 = _mix(key ^ idx)
+    x = np.ones(n)
+    y = np.zeros(n)
+    r2 = np.ones(n)
+    ok = np.zeros(n, dtype=bool)
+    for a in range(64):
+        todo = ~ok
+        if not todo.any():
+            break
+        xa = 2.0 * _u01(s0[todo], 2 * a) - 1.0
+        ya = 2.0 * _u01(s0[todo], 2 * a + 1) - 1.0
+        ra = xa * xa + ya * ya
+        acc = (ra <= 1.0) & (ra > 2.0 ** -60)
+        sel = np.nonzero(todo)[0]
+        x[sel] = xa
+        y[sel] = ya
+        r2[sel] = ra
+        ok[sel[acc]] = True
+    nrm = np.sqrt(r2)
+    dx = np.where(ok, x / nrm, 1.0)
+    dy = np.where(ok, y / nrm, 0.0)
+    x0, y0, x1, y1 = (float(v) for v in box)
+    W, H = x1 - x0, y1 - y0
+    if mode == MODE_INTERIOR:
+        ox = x0 + W * _u01(s0, 128)
+        oy = y0 + H * _u01(s0, 129)
+    else:
+        cx, cy = x0 + 0.5 * W, y0 + 0.5 * H
+        nx, ny = -dy, dx
+        w = 0.5 * (np.abs(nx) * W + np.abs(ny) * H)
+        s = w * (2.0 * _u01(s0, 128) - 1.0)
+        px, py = cx + s * nx, cy + s * ny
+        with np.errstate(divide="ignore", invalid="ignore"):
+            tx = np.where(dx > 0.0, (x0 - px) / dx, np.where(dx < 0.0, (x1 - px) / dx, -np.inf))
+            ty = np.where(dy > 0.0, (y0 - py) / dy, np.where(dy < 0.0, (y1 - py) / dy, -np.inf))
+        xside = tx >= ty
+        with np.errstate(invalid="ignore"):
+            oy_x = _clamp(py + tx * dy, y0, y1)
+            ox_y = _clamp(px + ty * dx, x0, x1)
+        ox = np.where(xside, np.where(dx > 0.0, x0, x1), ox_y)
+        oy = np.where(xside, oy_x, np.where(dy > 0.0, y0, y1))
+    return np.ascontiguousarray(np.stack([ox, oy, dx, dy], axis=1))

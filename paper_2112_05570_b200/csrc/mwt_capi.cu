@@ -1,0 +1,452 @@
+// extern "C" ABI of libmwt.so (declared in include/mwt.h).
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "mwt_internal.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+int cuda_fail(cudaError_t e, const char *where) {
+    g_err = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+    return MWT_E_CUDA;
+}
+
+#define CK(expr)                                                \
+    do {                                                        \
+        cudaError_t _e = (expr);                                \
+        if (_e != cudaSuccess) return cuda_fail(_e, #expr);     \
+    } while (0)
+
+// restores the caller's current device on scope exit
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = false;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) == cudaSuccess && (prev == dev || cudaSetDevice(dev) == cudaSuccess))
+            ok = true;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// one device allocation, carved into 256-B aligned pieces
+struct Arena {
+    char *base = nullptr;
+    size_t size = 0, used = 0;
+    static size_t align(size_t n) { return (n + 255) & ~size_t(255); }
+};
+
+template <typename T>
+T *carve(Arena &a, size_t count) {
+    T *p = reinterpret_cast<T *>(a.base + a.used);
+    a.used += Arena::align(count * sizeof(T));
+    return p;
+}
+
+}  // namespace
+
+struct mwt_mesh {
+    int device = 0;
+    mwt::MeshDev dev{};
+    mwt_mesh_info info{};
+    void *blob = nullptr;
+    // scratch for the host-buffer entry point
+    std::mutex mu;
+    void *scratch = nullptr;
+    size_t scratch_bytes = 0;
+    cudaStream_t stream = nullptr;
+};
+
+struct mwt_bvh {
+    const mwt_mesh *mesh = nullptr;
+    mwt::BvhDev dev{};
+    void *blob = nullptr;
+};
+
+struct mwt_kd {
+    const mwt_mesh *mesh = nullptr;
+    mwt::KdDev dev{};
+    void *blob = nullptr;
+};
+
+extern "C" {
+
+int mwt_abi_version(void) { return MWT_ABI_VERSION; }
+
+const char *mwt_last_error(void) { return g_err.c_str(); }
+
+int mwt_device_count(int *count) {
+    if (!count) return fail(MWT_E_INVALID, "device_count: NULL");
+    CK(cudaGetDeviceCount(count));
+    return MWT_OK;
+}
+
+int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const int32_t *tri_v,
+                    const int32_t *tri_nbr, const int32_t *tri_flag, int32_t ntris,
+                    const double *seg_xy, const uint8_t *seg_kind, int32_t nsegs, int device,
+                    mwt_mesh **out) {
+    if (!out) return fail(MWT_E_INVALID, "mesh_create: out is NULL");
+    *out = nullptr;
+    mwt::HostPacked P;
+    std::string err;
+    int rc = mwt::pack_mesh(vx, vy, nverts, tri_v, tri_nbr, tri_flag, ntris, seg_xy, seg_kind,
+                            nsegs, &P, &err);
+    if (rc != MWT_OK) return fail(rc, err);
+    DeviceGuard g(device);
+    if (!g.ok) return fail(MWT_E_CUDA, "mesh_create: cannot select device " + std::to_string(device));
+    const size_t nt = P.nt > 0 ? P.nt : 1, ns = P.ns > 0 ? P.ns : 1;
+    size_t bytes = Arena::align(nt * 16) + Arena::align(nt * 48) + Arena::align(nt * 16) +
+                   Arena::align(ns * 32) + Arena::align(ns) + Arena::align(ns * 2 * 8) +
+                   Arena::align(P.ep_ids.size() * 4) + Arena::align(P.anchor.size() * 4);
+    Arena a;
+    CK(cudaMalloc(&a.base, bytes));
+    a.size = bytes;
+    mwt_mesh *m = new mwt_mesh();
+    m->device = device;
+    m->blob = a.base;
+    int4 *link = carve<int4>(a, nt);
+    double2 *cxy = carve<double2>(a, 3 * nt);
+    int4 *lnbr = carve<int4>(a, nt);
+    double4 *seg = carve<double4>(a, ns);
+    uint8_t *kind = carve<uint8_t>(a, ns);
+    int2 *epr = carve<int2>(a, 2 * ns);
+    int32_t *epi = carve<int32_t>(a, P.ep_ids.size());
+    int32_t *anc = carve<int32_t>(a, P.anchor.size());
+    cudaError_t e = cudaSuccess;
+    auto up = [&](void *dst, const void *src, size_t n) {
+        if (e == cudaSuccess && n) e = cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
+    };
+    up(link, P.link.data(), (size_t)P.nt * 16);
+    up(cxy, P.cxy.data(), (size_t)P.nt * 48);
+    up(lnbr, P.lnbr.data(), (size_t)P.nt * 16);
+    up(seg, P.seg.data(), (size_t)P.ns * 32);
+    up(kind, P.segkind.data(), (size_t)P.ns);
+    up(epr, P.ep_range.data(), (size_t)P.ns * 16);
+    up(epi, P.ep_ids.data(), P.ep_ids.size() * 4);
+    up(anc, P.anchor.data(), P.anchor.size() * 4);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) {
+        cudaFree(a.base);
+        delete m;
+        return cuda_fail(e, "mesh_create: upload");
+    }
+    m->dev = mwt::MeshDev{P.nt, P.ns, P.res, link, cxy, lnbr, seg, kind, epr, epi, anc};
+    m->info.num_vertices = P.nv;
+    m->info.num_triangles = P.nt;
+    m->info.num_segments = P.ns;
+    m->info.anchor_res = P.res;
+    m->info.anchors_not_strict = P.anchors_not_strict;
+    m->info.device = device;
+    m->info.device_bytes = (int64_t)bytes;
+    m->info.walk_record_bytes = 32;
+    *out = m;
+    return MWT_OK;
+}
+
+int mwt_mesh_destroy(mwt_mesh *m) {
+    if (!m) return MWT_OK;
+    DeviceGuard g(m->device);
+    if (m->stream) cudaStreamDestroy(m->stream);
+    if (m->scratch) cudaFree(m->scratch);
+    if (m->blob) cudaFree(m->blob);
+    delete m;
+    return MWT_OK;
+}
+
+int mwt_mesh_info_get(const mwt_mesh *m, mwt_mesh_info *out) {
+    if (!m || !out) return fail(MWT_E_INVALID, "mesh_info: NULL");
+    *out = m->info;
+    return MWT_OK;
+}
+
+int mwt_mesh_anchors(const mwt_mesh *m, int32_t *out_host) {
+    if (!m || !out_host) return fail(MWT_E_INVALID, "mesh_anchors: NULL");
+    DeviceGuard g(m->device);
+    if (m->dev.res > 0)
+        CK(cudaMemcpy(out_host, m->dev.anchor, sizeof(int32_t) * m->dev.res * m->dev.res,
+                      cudaMemcpyDeviceToHost));
+    return MWT_OK;
+}
+
+int mwt_raygen_dev(int mode, const double *box, uint64_t seed, uint64_t first, int64_t n,
+                   double *rays_out, void *stream) {
+    if (!box || (n > 0 && !rays_out) || n < 0 || (mode != MWT_RAYS_BOX_ENTRY && mode != MWT_RAYS_INTERIOR))
+        return fail(MWT_E_INVALID, "raygen: bad argument");
+    int rc = mwt::launch_raygen(mode, box, seed, first, n, rays_out, stream);
+    if (rc) return cuda_fail((cudaError_t)rc, "raygen launch");
+    return MWT_OK;
+}
+
+int mwt_locate_dev(const mwt_mesh *m, const double *pts, int64_t n, int32_t *out_tid,
+                   uint32_t *out_status, void *stream) {
+    if (!m || n < 0 || (n > 0 && !pts)) return fail(MWT_E_INVALID, "locate: bad argument");
+    if (m->dev.nt == 0) return fail(MWT_E_INVALID, "locate: mesh has no triangles");
+    DeviceGuard g(m->device);
+    int rc = mwt::launch_locate(m->dev, pts, n, out_tid, out_status, stream);
+    if (rc) return cuda_fail((cudaError_t)rc, "locate launch");
+    return MWT_OK;
+}
+
+int mwt_trace_dev(const mwt_mesh *m, const double *rays, const int32_t *start, int64_t n,
+                  int32_t *out_start, int32_t *out_seg, double *out_t, double *out_u,
+                  int32_t *out_steps, uint32_t *out_status, void *stream) {
+    if (!m || n < 0 || (n > 0 && !rays)) return fail(MWT_E_INVALID, "trace: bad argument");
+    if (m->dev.nt == 0) return fail(MWT_E_INVALID, "trace: mesh has no triangles");
+    DeviceGuard g(m->device);
+    int rc = mwt::launch_trace(m->dev, rays, start, n, out_start, out_seg, out_t, out_u, out_steps,
+                               out_status, stream);
+    if (rc) return cuda_fail((cudaError_t)rc, "trace launch");
+    return MWT_OK;
+}
+
+int mwt_trace_host(const mwt_mesh *cm, const double *rays, const int32_t *start, int64_t n,
+                   int32_t *out_start, int32_t *out_seg, double *out_t, double *out_u,
+                   int32_t *out_steps, uint32_t *out_status) {
+    mwt_mesh *m = const_cast<mwt_mesh *>(cm);
+    if (!m || n < 0 || (n > 0 && !rays)) return fail(MWT_E_INVALID, "trace_host: bad argument");
+    if (m->dev.nt == 0) return fail(MWT_E_INVALID, "trace_host: mesh has no triangles");
+    if (n == 0) return MWT_OK;
+    std::lock_guard<std::mutex> lk(m->mu);
+    DeviceGuard g(m->device);
+    // per-ray device bytes: rays 32 + start 4 + outputs 4+4+8+8+4+4
+    const size_t per = 32 + 4 + 4 + 4 + 8 + 8 + 4 + 4;
+    size_t need = (size_t)n * per + 8 * 256;
+    if (need > m->scratch_bytes) {
+        if (m->scratch) cudaFree(m->scratch);
+        m->scratch = nullptr;
+        m->scratch_bytes = 0;
+        CK(cudaMalloc(&m->scratch, need));
+        m->scratch_bytes = need;
+    }
+    Arena a;
+    a.base = (char *)m->scratch;
+    a.size = need;
+    double *d_rays = carve<double>(a, 4 * n);
+    int32_t *d_start = carve<int32_t>(a, n);
+    int32_t *d_ostart = carve<int32_t>(a, n);
+    int32_t *d_seg = carve<int32_t>(a, n);
+    double *d_t = carve<double>(a, n);
+    double *d_u = carve<double>(a, n);
+    int32_t *d_steps = carve<int32_t>(a, n);
+    uint32_t *d_st = carve<uint32_t>(a, n);
+    cudaStream_t s = m->stream;
+    CK(cudaMemcpyAsync(d_rays, rays, 32 * (size_t)n, cudaMemcpyHostToDevice, s));
+    if (start) CK(cudaMemcpyAsync(d_start, start, 4 * (size_t)n, cudaMemcpyHostToDevice, s));
+    int rc = mwt::launch_trace(m->dev, d_rays, start ? d_start : nullptr, n,
+                               out_start ? d_ostart : nullptr, out_seg ? d_seg : nullptr,
+                               out_t ? d_t : nullptr, out_u ? d_u : nullptr,
+                               out_steps ? d_steps : nullptr, out_status ? d_st : nullptr, s);
+    if (rc) return cuda_fail((cudaError_t)rc, "trace_host launch");
+    if (out_start) CK(cudaMemcpyAsync(out_start, d_ostart, 4 * (size_t)n, cudaMemcpyDeviceToHost, s));
+    if (out_seg) CK(cudaMemcpyAsync(out_seg, d_seg, 4 * (size_t)n, cudaMemcpyDeviceToHost, s));
+    if (out_t) CK(cudaMemcpyAsync(out_t, d_t, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));
+    if (out_u) CK(cudaMemcpyAsync(out_u, d_u, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));
+    if (out_steps) CK(cudaMemcpyAsync(out_steps, d_steps, 4 * (size_t)n, cudaMemcpyDeviceToHost, s));
+    if (out_status) CK(cudaMemcpyAsync(out_status, d_st, 4 * (size_t)n, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return MWT_OK;
+}
+
+int mwt_trace_generated_dev(const mwt_mesh *m, int mode, const double *box, uint64_t seed,
+                            uint64_t first, int64_t n, int32_t *out_seg, double *out_t,
+                            int32_t *out_steps, int64_t *hist, void *stream) {
+    if (!m || !box || n < 0 || (mode != MWT_RAYS_BOX_ENTRY && mode != MWT_RAYS_INTERIOR))
+        return fail(MWT_E_INVALID, "trace_generated: bad argument");
+    if (m->dev.nt == 0) return fail(MWT_E_INVALID, "trace_generated: mesh has no triangles");
+    DeviceGuard g(m->device);
+    int rc = mwt::launch_trace_generated(m->dev, mode, box, seed, first, n, out_seg, out_t,
+                                         out_steps, reinterpret_cast<long long *>(hist), stream);
+    if (rc) return cuda_fail((cudaError_t)rc, "trace_generated launch");
+    return MWT_OK;
+}
+
+int mwt_histogram_dev(const int32_t *seg, const int32_t *steps, const uint32_t *status, int64_t n,
+                      int64_t *hist, void *stream) {
+    if (n < 0 || (n > 0 && (!seg || !steps || !hist))) return fail(MWT_E_INVALID, "histogram: bad argument");
+    int rc = mwt::launch_histogram(seg, steps, status, n, reinterpret_cast<long long *>(hist), stream);
+    if (rc) return cuda_fail((cudaError_t)rc, "histogram launch");
+    return MWT_OK;
+}
+
+int mwt_bvh_create(const mwt_mesh *mesh, int32_t nnodes, const double *box, const int32_t *left,
+                   const int32_t *right, const int32_t *prim_off, const int32_t *prim_cnt,
+                   int32_t nprims, const int32_t *prims, mwt_bvh **out) {
+    if (!mesh || !out || nnodes <= 0 || !box || !left || !right || !prim_off || !prim_cnt ||
+        nprims < 0 || (nprims > 0 && !prims))
+        return fail(MWT_E_INVALID, "bvh_create: bad argument");
+    *out = nullptr;
+    for (int k = 0; k < nnodes; k++) {
+        bool leaf = left[k] < 0;
+        if ((leaf && (prim_off[k] < 0 || prim_cnt[k] < 0 || prim_off[k] + prim_cnt[k] > nprims)) ||
+            (!leaf && (left[k] >= nnodes || right[k] < 0 || right[k] >= nnodes)))
+            return fail(MWT_E_INVALID, "bvh_create: node " + std::to_string(k) + " out of range");
+    }
+    for (int k = 0; k < nprims; k++)
+        if (prims[k] < 0 || prims[k] >= mesh->dev.ns)
+            return fail(MWT_E_INVALID, "bvh_create: primitive id out of range");
+    DeviceGuard g(mesh->device);
+    std::vector<int32_t> child(2 * (size_t)nnodes), pr(2 * (size_t)nnodes);
+    for (int k = 0; k < nnodes; k++) {
+        child[2 * k] = left[k];
+        child[2 * k + 1] = right[k];
+        pr[2 * k] = prim_off[k];
+        pr[2 * k + 1] = prim_cnt[k];
+    }
+    size_t np = nprims > 0 ? nprims : 1;
+    size_t bytes = Arena::align(32 * (size_t)nnodes) + 2 * Arena::align(8 * (size_t)nnodes) +
+                   Arena::align(4 * np);
+    Arena a;
+    CK(cudaMalloc(&a.base, bytes));
+    mwt_bvh *b = new mwt_bvh();
+    b->mesh = mesh;
+    b->blob = a.base;
+    double4 *dbox = carve<double4>(a, nnodes);
+    int2 *dch = carve<int2>(a, nnodes);
+    int2 *dpr = carve<int2>(a, nnodes);
+    int32_t *dpm = carve<int32_t>(a, np);
+    cudaError_t e = cudaMemcpy(dbox, box, 32 * (size_t)nnodes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dch, child.data(), 8 * (size_t)nnodes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dpr, pr.data(), 8 * (size_t)nnodes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && nprims > 0) e = cudaMemcpy(dpm, prims, 4 * (size_t)nprims, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+        cudaFree(a.base);
+        delete b;
+        return cuda_fail(e, "bvh_create: upload");
+    }
+    b->dev = mwt::BvhDev{nnodes, dbox, dch, dpr, dpm};
+    *out = b;
+    return MWT_OK;
+}
+
+int mwt_bvh_destroy(mwt_bvh *b) {
+    if (!b) return MWT_OK;
+    DeviceGuard g(b->mesh->device);
+    cudaFree(b->blob);
+    delete b;
+    return MWT_OK;
+}
+
+int mwt_bvh_trace_dev(const mwt_bvh *b, const double *rays, int64_t n, int32_t *out_seg,
+                      double *out_t, double *out_u, int32_t *out_node_tests,
+                      int32_t *out_prim_tests, uint32_t *out_status, void *stream) {
+    if (!b || n < 0 || (n > 0 && !rays)) return fail(MWT_E_INVALID, "bvh_trace: bad argument");
+    DeviceGuard g(b->mesh->device);
+    int rc = mwt::launch_bvh(b->mesh->dev, b->dev, rays, n, out_seg, out_t, out_u, out_node_tests,
+                             out_prim_tests, out_status, stream);
+    if (rc) return cuda_fail((cudaError_t)rc, "bvh_trace launch");
+    return MWT_OK;
+}
+
+int mwt_kd_create(const mwt_mesh *mesh, int32_t nnodes, int32_t num_leaves, const int32_t *axis,
+                  const double *pos, const int32_t *left, const int32_t *right, const double *box,
+                  const int32_t *ropes, const int32_t *rope_cost, const int32_t *prim_off,
+                  const int32_t *prim_cnt, int32_t nprims, const int32_t *prims, mwt_kd **out) {
+    if (!mesh || !out || nnodes <= 0 || num_leaves <= 0 || !axis || !pos || !left || !right ||
+        !box || !ropes || !rope_cost || !prim_off || !prim_cnt || nprims < 0 || (nprims > 0 && !prims))
+        return fail(MWT_E_INVALID, "kd_create: bad argument");
+    *out = nullptr;
+    for (int k = 0; k < nnodes; k++) {
+        if (axis[k] >= 0) {
+            if (axis[k] > 1 || left[k] < 0 || left[k] >= nnodes || right[k] < 0 || right[k] >= nnodes)
+                return fail(MWT_E_INVALID, "kd_create: node " + std::to_string(k) + " out of range");
+        } else {
+            if (prim_off[k] < 0 || prim_cnt[k] < 0 || prim_off[k] + prim_cnt[k] > nprims)
+                return fail(MWT_E_INVALID, "kd_create: leaf " + std::to_string(k) + " prims out of range");
+            for (int s = 0; s < 4; s++)
+                if (ropes[4 * k + s] < -1 || ropes[4 * k + s] >= nnodes)
+                    return fail(MWT_E_INVALID, "kd_create: rope out of range");
+        }
+    }
+    for (int k = 0; k < nprims; k++)
+        if (prims[k] < 0 || prims[k] >= mesh->dev.ns)
+            return fail(MWT_E_INVALID, "kd_create: primitive id out of range");
+    DeviceGuard g(mesh->device);
+    std::vector<int32_t> child(2 * (size_t)nnodes), pr(2 * (size_t)nnodes);
+    for (int k = 0; k < nnodes; k++) {
+        child[2 * k] = left[k];
+        child[2 * k + 1] = right[k];
+        pr[2 * k] = prim_off[k];
+        pr[2 * k + 1] = prim_cnt[k];
+    }
+    size_t np = nprims > 0 ? nprims : 1, nn = nnodes;
+    size_t bytes = Arena::align(4 * nn) + Arena::align(8 * nn) + Arena::align(8 * nn) +
+                   Arena::align(32 * nn) + 2 * Arena::align(16 * nn) + Arena::align(8 * nn) +
+                   Arena::align(4 * np);
+    Arena a;
+    CK(cudaMalloc(&a.base, bytes));
+    mwt_kd *k = new mwt_kd();
+    k->mesh = mesh;
+    k->blob = a.base;
+    int32_t *dax = carve<int32_t>(a, nn);
+    double *dpos = carve<double>(a, nn);
+    int2 *dch = carve<int2>(a, nn);
+    double4 *dbox = carve<double4>(a, nn);
+    int4 *drope = carve<int4>(a, nn);
+    int4 *dcost = carve<int4>(a, nn);
+    int2 *dpr = carve<int2>(a, nn);
+    int32_t *dpm = carve<int32_t>(a, np);
+    cudaError_t e = cudaSuccess;
+    auto up = [&](void *dst, const void *src, size_t n) {
+        if (e == cudaSuccess && n) e = cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
+    };
+    up(dax, axis, 4 * nn);
+    up(dpos, pos, 8 * nn);
+    up(dch, child.data(), 8 * nn);
+    up(dbox, box, 32 * nn);
+    up(drope, ropes, 16 * nn);
+    up(dcost, rope_cost, 16 * nn);
+    up(dpr, pr.data(), 8 * nn);
+    up(dpm, prims, 4 * (size_t)nprims);
+    if (e != cudaSuccess) {
+        cudaFree(a.base);
+        delete k;
+        return cuda_fail(e, "kd_create: upload");
+    }
+    k->dev = mwt::KdDev{nnodes, num_leaves, dax, dpos, dch, dbox, drope, dcost, dpr, dpm};
+    *out = k;
+    return MWT_OK;
+}
+
+int mwt_kd_destroy(mwt_kd *k) {
+    if (!k) return MWT_OK;
+    DeviceGuard g(k->mesh->device);
+    cudaFree(k->blob);
+    delete k;
+    return MWT_OK;
+}
+
+int mwt_kd_trace_dev(const mwt_kd *k, const double *rays, int64_t n, int32_t *out_seg,
+                     double *out_t, double *out_u, int32_t *out_nodes, int32_t *out_rope_steps,
+                     int32_t *out_prim_tests, uint32_t *out_status, void *stream) {
+    if (!k || n < 0 || (n > 0 && !rays)) return fail(MWT_E_INVALID, "kd_trace: bad argument");
+    DeviceGuard g(k->mesh->device);
+    int rc = mwt::launch_kd(k->mesh->dev, k->dev, rays, n, out_seg, out_t, out_u, out_nodes,
+                            out_rope_steps, out_prim_tests, out_status, stream);
+    if (rc) return cuda_fail((cudaError_t)rc, "kd_trace launch");
+    return MWT_OK;
+}
+
+int mwt_brute_force_dev(const mwt_mesh *m, const double *rays, int64_t n, int32_t *out_seg,
+                        double *out_t, double *out_u, void *stream) {
+    if (!m || n < 0 || (n > 0 && !rays)) return fail(MWT_E_INVALID, "brute_force: bad argument");
+    DeviceGuard g(m->device);
+    int rc = mwt::launch_brute(m->dev, rays, n, out_seg, out_t, out_u, stream);
+    if (rc) return cuda_fail((cudaError_t)rc, "brute_force launch");
+    return MWT_OK;
+}
+
+}  // extern "C"

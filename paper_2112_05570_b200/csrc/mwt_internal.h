@@ -1,0 +1,120 @@
+// Internal structures shared by the host packer (mwt_pack.cpp), the kernels
+// (mwt_kernels.cu) and the C ABI (mwt_capi.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <vector_types.h>
+
+#include "mwt.h"
+
+namespace mwt {
+
+// ---------------------------------------------------------------------------
+// Packed triangulation (K1).  Layout in HBM (all arrays 16-B aligned):
+//
+//   link[T]   int4  walk words, one per edge i = 0..2 (edge i is opposite
+//                   corner i, endpoints corners (i+1)%3, (i+2)%3 -- trimesh.py:10-13):
+//                     bit31 = 0  : internal edge, (nbr << 2) | mirror j
+//                     bit31 = 1  : walk stops here; bit30 = boundary kind,
+//                                  bits 0..29 = scene segment id (geometry hit)
+//                     0xFFFFFFFF : internal edge without neighbour (miss)
+//                   .w = 0 (pad)
+//   cxy[3T]   double2 corner coordinates (x, y) of corner k of triangle t
+//                   at 3t+k: the one vertex a walk step does not already know
+//                   is corner j of the neighbour -> ONE 16-B load, independent
+//                   of the 16-B link load.
+//   lnbr[T]   int4  locate words: (nbr << 2) | mirror for every neighbour,
+//                   across constrained edges too; -1 = None.  Read only by
+//                   point location (accel.py:291-330 ignores flags).
+//   seg[S]    double4 (ax, ay, bx, by); segkind[S] uint8 (0 G, 1 B)
+//   ep_range[2S] int2 (offset, count) into ep_ids: for endpoint e of
+//                   segment s (2s = a, 2s+1 = b), the ascending geometry
+//                   segment ids sharing that exact point (SceneIndex.endpoint_map).
+//   anchor[res*res] int32 TriLocator anchor triangles, row-major (cy, cx).
+//
+// One walk step reads link[N] (16 B) + cxy[3N+j] (16 B) = 32 algorithmic B.
+// ---------------------------------------------------------------------------
+
+constexpr uint32_t kStopBit = 0x80000000u;
+constexpr uint32_t kBoundaryBit = 0x40000000u;
+constexpr uint32_t kOpenWord = 0xFFFFFFFFu;
+constexpr uint32_t kSidMask = 0x3FFFFFFFu;
+
+struct HostPacked {
+    int32_t nv = 0, nt = 0, ns = 0;
+    int32_t res = 0, anchors_not_strict = 0;
+    std::vector<int32_t> link;      // 4*nt
+    std::vector<double> cxy;        // 6*nt
+    std::vector<int32_t> lnbr;      // 4*nt
+    std::vector<double> seg;        // 4*ns
+    std::vector<uint8_t> segkind;   // ns
+    std::vector<int32_t> ep_range;  // 2*(2*ns)
+    std::vector<int32_t> ep_ids;
+    std::vector<int32_t> anchor;    // res*res
+};
+
+// Build the packed layout; returns MWT_OK or an error code with *err set.
+int pack_mesh(const double *vx, const double *vy, int32_t nverts, const int32_t *tri_v,
+              const int32_t *tri_nbr, const int32_t *tri_flag, int32_t ntris,
+              const double *seg_xy, const uint8_t *seg_kind, int32_t nsegs, HostPacked *out,
+              std::string *err);
+
+// Device view passed by value to kernels.
+struct MeshDev {
+    int32_t nt, ns, res;
+    const int4 *link;
+    const double2 *cxy;
+    const int4 *lnbr;
+    const double4 *seg;
+    const uint8_t *segkind;
+    const int2 *ep_range;
+    const int32_t *ep_ids;
+    const int32_t *anchor;
+};
+
+struct BvhDev {
+    int32_t nnodes;
+    const double4 *box;
+    const int2 *child;     // (left, right), left < 0 => leaf
+    const int2 *prange;    // (prim_off, prim_cnt)
+    const int32_t *prims;
+};
+
+struct KdDev {
+    int32_t nnodes, nleaves;
+    const int32_t *axis;
+    const double *pos;
+    const int2 *child;
+    const double4 *box;
+    const int4 *ropes;
+    const int4 *rope_cost;
+    const int2 *prange;
+    const int32_t *prims;
+};
+
+// launchers (mwt_kernels.cu); return cudaError_t as int
+int launch_raygen(int mode, const double *box, uint64_t seed, uint64_t first, int64_t n,
+                  double *rays, void *stream);
+int launch_locate(const MeshDev &m, const double *pts, int64_t n, int32_t *tid, uint32_t *st,
+                  void *stream);
+int launch_trace(const MeshDev &m, const double *rays, const int32_t *start, int64_t n,
+                 int32_t *o_start, int32_t *o_seg, double *o_t, double *o_u, int32_t *o_steps,
+                 uint32_t *o_st, void *stream);
+int launch_trace_generated(const MeshDev &m, int mode, const double *box, uint64_t seed,
+                           uint64_t first, int64_t n, int32_t *o_seg, double *o_t,
+                           int32_t *o_steps, long long *hist, void *stream);
+int launch_histogram(const int32_t *seg, const int32_t *steps, const uint32_t *st, int64_t n,
+                     long long *hist, void *stream);
+int launch_bvh(const MeshDev &m, const BvhDev &b, const double *rays, int64_t n, int32_t *o_seg,
+               double *o_t, double *o_u, int32_t *o_nodes, int32_t *o_prims, uint32_t *o_st,
+               void *stream);
+int launch_kd(const MeshDev &m, const KdDev &k, const double *rays, int64_t n, int32_t *o_seg,
+              double *o_t, double *o_u, int32_t *o_nodes, int32_t *o_ropes, int32_t *o_prims,
+              uint32_t *o_st, void *stream);
+int launch_brute(const MeshDev &m, const double *rays, int64_t n, int32_t *o_seg, double *o_t,
+                 double *o_u, void *stream);
+
+}  // namespace mwt

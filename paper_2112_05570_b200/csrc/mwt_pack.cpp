@@ -1,0 +1,200 @@
+// K1 -- host mesh packer: reference triangulation + scene -> device layout.
+//
+// Input is the reference data model as loaded by load_triangulation
+// (trimesh.py:1309-1337) and parse_scene (scene.py:135-165).  The packer
+//  * validates indices and neighbour symmetry (the subset of
+//    Triangulation.validate_topology, trimesh.py:283-311, the walk relies on),
+//  * computes each internal edge's mirror index (Triangulation.mirror,
+//    trimesh.py:154-163) so the walk skips its entry edge by index -- on a
+//    valid mesh identical to the reference's vertex-set test (accel.py:178),
+//  * builds SceneIndex.endpoint_map (accel.py:77-80) as per-endpoint ranges,
+//  * fills TriLocator's anchor grid (accel.py:263-282) with
+//    Triangulation.locate (trimesh.py:386-416), eagerly in row-major order.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "mwt_internal.h"
+
+namespace mwt {
+namespace {
+
+inline double sa2(double ax, double ay, double bx, double by, double cx, double cy) {
+    // geometry.py:81-83; this TU is compiled with -ffp-contract=off
+    return (bx - ax) * (cy - ay) - (by - ay) * (cx - ax);
+}
+
+struct Ctx {
+    const double *vx, *vy;
+    const int32_t *tv, *tn;
+    int32_t nt;
+};
+
+bool contains(const Ctx &c, int tid, double px, double py) {
+    const int32_t *v = c.tv + 3 * tid;
+    for (int i = 0; i < 3; i++) {
+        int a = v[(i + 1) % 3], b = v[(i + 2) % 3];
+        if (!(sa2(c.vx[a], c.vy[a], c.vx[b], c.vy[b], px, py) >= -1e-15)) return false;
+    }
+    return true;
+}
+
+// trimesh.py:386-416; returns tid, sets *strict when p is strictly inside
+int tri_locate(const Ctx &c, double px, double py, int hint, bool *strict) {
+    int tid = (hint >= 0 && hint < c.nt) ? hint : 0;
+    long cap = 4L * c.nt + 16;
+    for (long visited = 0; visited < cap; visited++) {
+        const int32_t *v = c.tv + 3 * tid;
+        int worst = -1;
+        double worst_val = 0.0;
+        bool all_pos = true;
+        for (int i = 0; i < 3; i++) {
+            int a = v[(i + 1) % 3], b = v[(i + 2) % 3];
+            double s = sa2(c.vx[a], c.vy[a], c.vx[b], c.vy[b], px, py);
+            if (!(s > 0.0)) all_pos = false;
+            if (s < worst_val) {
+                worst_val = s;
+                worst = i;
+            }
+        }
+        if (worst < 0) {
+            *strict = all_pos;
+            return tid;
+        }
+        int n = c.tn[3 * tid + worst];
+        if (n < 0) {
+            *strict = false;
+            return tid;
+        }
+        tid = n;
+    }
+    *strict = false;
+    for (int t = 0; t < c.nt; t++)  // _locate_scan, trimesh.py:428-436
+        if (contains(c, t, px, py)) return t;
+    return 0;
+}
+
+}  // namespace
+
+int pack_mesh(const double *vx, const double *vy, int32_t nv, const int32_t *tv, const int32_t *tn,
+              const int32_t *tf, int32_t nt, const double *seg_xy, const uint8_t *seg_kind,
+              int32_t ns, HostPacked *out, std::string *err) {
+    if (nt < 0 || nv < 0 || ns < 0 || (nt > 0 && (!vx || !vy || !tv || !tn || !tf)) ||
+        (ns > 0 && (!seg_xy || !seg_kind))) {
+        *err = "mesh_create: negative count or NULL array";
+        return MWT_E_INVALID;
+    }
+    if (nt >= (1 << 29) || ns >= (1 << 30)) {
+        *err = "mesh_create: triangulation too large for the 30-bit edge words";
+        return MWT_E_INVALID;
+    }
+    HostPacked &P = *out;
+    P.nv = nv;
+    P.nt = nt;
+    P.ns = ns;
+    for (int64_t k = 0; k < 3LL * nt; k++) {
+        if (tv[k] < 0 || tv[k] >= nv || tn[k] < -1 || tn[k] >= nt || tf[k] < -1 || tf[k] >= ns) {
+            *err = "mesh_create: index out of range in triangle " + std::to_string(k / 3);
+            return MWT_E_INVALID;
+        }
+    }
+    P.link.assign(4LL * nt, 0);
+    P.lnbr.assign(4LL * nt, -1);
+    P.cxy.resize(6LL * nt);
+    for (int t = 0; t < nt; t++) {
+        const int32_t *v = tv + 3 * t;
+        for (int k = 0; k < 3; k++) {
+            P.cxy[6LL * t + 2 * k] = vx[v[k]];
+            P.cxy[6LL * t + 2 * k + 1] = vy[v[k]];
+        }
+        for (int i = 0; i < 3; i++) {
+            int a = v[(i + 1) % 3], b = v[(i + 2) % 3];
+            int n = tn[3 * t + i];
+            int j = -1;
+            if (n >= 0) {
+                const int32_t *u = tv + 3 * n;
+                for (int jj = 0; jj < 3; jj++)
+                    if (u[(jj + 1) % 3] == b && u[(jj + 2) % 3] == a) j = jj;
+                if (j < 0 || tn[3 * n + j] != t) {
+                    *err = "mesh_create: neighbor symmetry broken at " + std::to_string(t) + ":" +
+                           std::to_string(i) + " -> " + std::to_string(n);
+                    return MWT_E_TOPOLOGY;
+                }
+                P.lnbr[4LL * t + i] = (n << 2) | j;
+            }
+            int f = tf[3 * t + i];
+            uint32_t w;
+            if (f != -1) {
+                w = kStopBit | (seg_kind[f] ? kBoundaryBit : 0u) | (uint32_t)f;
+            } else if (n < 0) {
+                w = kOpenWord;
+            } else {
+                w = ((uint32_t)n << 2) | (uint32_t)j;
+            }
+            P.link[4LL * t + i] = (int32_t)w;
+        }
+    }
+    P.seg.assign(seg_xy, seg_xy + 4LL * ns);
+    P.segkind.assign(seg_kind, seg_kind + ns);
+
+    // SceneIndex.endpoint_map: exact (x, y) -> ascending geometry sids
+    struct Ep {
+        double x, y;
+        int32_t sid, end;
+    };
+    std::vector<Ep> eps;
+    for (int s = 0; s < ns; s++) {
+        if (seg_kind[s] != 0) continue;
+        eps.push_back({seg_xy[4LL * s], seg_xy[4LL * s + 1], s, 0});
+        eps.push_back({seg_xy[4LL * s + 2], seg_xy[4LL * s + 3], s, 1});
+    }
+    std::sort(eps.begin(), eps.end(), [](const Ep &p, const Ep &q) {
+        if (p.x < q.x) return true;
+        if (q.x < p.x) return false;
+        if (p.y < q.y) return true;
+        if (q.y < p.y) return false;
+        return p.sid < q.sid;
+    });
+    P.ep_range.assign(4LL * ns, 0);
+    P.ep_ids.clear();
+    for (size_t g = 0; g < eps.size();) {
+        size_t h = g;
+        while (h < eps.size() && eps[h].x == eps[g].x && eps[h].y == eps[g].y) h++;
+        int32_t off = (int32_t)P.ep_ids.size();
+        for (size_t k = g; k < h; k++) P.ep_ids.push_back(eps[k].sid);
+        for (size_t k = g; k < h; k++) {
+            int e = 2 * eps[k].sid + eps[k].end;
+            P.ep_range[2LL * e] = off;
+            P.ep_range[2LL * e + 1] = (int32_t)(h - g);
+        }
+        g = h;
+    }
+    if (P.ep_ids.empty()) P.ep_ids.push_back(0);
+
+    if (nt == 0) {  // scene-only mesh (BVH / kd / brute force); no walk, no locate
+        P.res = 0;
+        P.anchor.assign(1, 0);
+        return MWT_OK;
+    }
+    // TriLocator anchors, accel.py:263-282
+    int ntc = nt > 4 ? nt : 4;
+    int res = (int)std::sqrt(ntc / 2.0);
+    if (res < 2) res = 2;
+    P.res = res;
+    P.anchor.assign((size_t)res * res, 0);
+    P.anchors_not_strict = 0;
+    Ctx c{vx, vy, tv, tn, nt};
+    int hint = -1;
+    for (int cy = 0; cy < res; cy++)
+        for (int cx = 0; cx < res; cx++) {
+            double px = (cx + 0.5) / res, py = (cy + 0.5) / res;
+            bool strict = false;
+            int tid = tri_locate(c, px, py, hint, &strict);
+            if (!strict) P.anchors_not_strict++;
+            hint = tid;
+            P.anchor[(size_t)cy * res + cx] = tid;
+        }
+    return MWT_OK;
+}
+
+}  // namespace mwt

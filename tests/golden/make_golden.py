@@ -1,0 +1,296 @@
+"""Generate the golden vectors that pin the oracle (and the engine) to the
+reference.  Runs ONLY in the build container: it imports the unmodified
+reference package from /root/reference/pkg/src (and its test helpers from
+/root/reference/pkg/tests/conftest.py) and records what the reference itself
+returns.  Outputs (committed): tests/golden/*.npz.
+
+  known.npz     hand-built and reference-test cases (test_accel.py, test_geometry.py)
+  config_<c>.npz  per BASELINE config: rays, reference start/seg/t/u/steps on cdt & mwt
+  struct_<c>.npz  per config: reference bvh/kd results + counters on a ray subset
+  hypot.npz     math.hypot values (CPython's is correctly rounded)
+
+Usage: python tests/golden/make_golden.py [group ...]
+"""
+from __future__ import annotations
+
+import math
+import os
+import random
+import sys
+import tempfile
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path[:0] = ["/root/reference/pkg/src", "/root/reference/pkg/tests", ROOT]
+
+from mintri.geometry import Point, Ray, Segment, ray_segment_intersect  # noqa: E402
+from mintri.scene import Scene  # noqa: E402
+from mintri.trimesh import build_cdt, load_triangulation, refine_cdt, save_triangulation  # noqa: E402
+from mintri.accel import (SceneIndex, TraversalError, TriLocator, brute_force_closest,  # noqa: E402
+                          build_bvh, build_kdtree, bvh_intersect, kd_intersect,
+                          locate_triangle, traverse_triangulation)
+from mintri.experiment import sample_rays  # noqa: E402
+from conftest import random_segment_scene  # noqa: E402  (reference tests/conftest.py:10-42)
+
+from oracle.raygen import raygen  # noqa: E402
+
+CONFIGS = ["lines64", "lines1024", "grass4096", "hair512", "floorplan64"]
+BOXES = {"grass4096": (0.0, 0.0, 1.0, 0.5)}
+FIX = os.path.join(ROOT, "fixtures", "data")
+
+
+def roundtrip(tri):
+    """save + load: compact ids exactly as the engine and oracle see them."""
+    with tempfile.TemporaryDirectory() as d:
+        p = os.path.join(d, "t.tri")
+        save_triangulation(tri, p)
+        return load_triangulation(p, tri.scene)
+
+
+def scene_arrays(scene):
+    xy = np.array([[s.a.x, s.a.y, s.b.x, s.b.y] for s in scene.segments], np.float64).reshape(-1, 4)
+    kind = np.array([0 if s.kind.value == "G" else 1 for s in scene.segments], np.uint8)
+    return xy, kind
+
+
+def tri_arrays(tri):
+    vxy = np.array([[v.x, v.y] for v in tri.verts], np.float64).reshape(-1, 2)
+    v = np.array([t.v for t in tri.tris], np.int32).reshape(-1, 3)
+    nbr = np.array([[-1 if n is None else n for n in t.nbr] for t in tri.tris], np.int32).reshape(-1, 3)
+    flag = np.array([t.flag for t in tri.tris], np.int32).reshape(-1, 3)
+    return vxy, v, nbr, flag
+
+
+def ray_arr(rays):
+    return np.array([[r.origin.x, r.origin.y, r.direction.x, r.direction.y] for r in rays],
+                    np.float64).reshape(-1, 4)
+
+
+def run_walk(tri, rays, starts=None, index=None):
+    """Reference TriLocator.locate + traverse_triangulation per ray."""
+    index = index or SceneIndex(tri.scene)
+    loc = TriLocator(tri)
+    n = len(rays)
+    out = dict(start=np.empty(n, np.int32), seg=np.full(n, -1, np.int32), t=np.full(n, np.nan),
+               u=np.full(n, np.nan), steps=np.zeros(n, np.int32), error=np.zeros(n, np.uint8))
+    for i, r in enumerate(rays):
+        s = loc.locate(r.origin) if starts is None else int(starts[i])
+        out["start"][i] = s
+        try:
+            hit, st = traverse_triangulation(tri, r, s, index)
+        except TraversalError:
+            out["error"][i] = 1
+            continue
+        out["steps"][i] = st.tri_steps
+        if hit is not None:
+            out["seg"][i] = hit.seg
+            out["t"][i] = hit.t
+            seg = tri.scene.segments[hit.seg]
+            # recover u from the hit point (point_at(u) is what the reference stores)
+            ex, ey = seg.b.x - seg.a.x, seg.b.y - seg.a.y
+            out["u"][i] = ((hit.point.x - seg.a.x) * ex + (hit.point.y - seg.a.y) * ey) / (ex * ex + ey * ey)
+    return out
+
+
+def prefixed(prefix, d):
+    return {f"{prefix}{k}": v for k, v in d.items()}
+
+
+def rays_from(arr):
+    return [Ray(Point(float(a), float(b)), Point(float(c), float(d))) for a, b, c, d in arr]
+
+
+# ----------------------------------------------------------------------
+
+def make_known():
+    out = {}
+    cases = []
+
+    # test_accel.py:40-44 empty square
+    sc = Scene.from_geometry([], name="empty")
+    cases.append(("empty", sc, [Ray(Point(0.5, 0.5), Point(1, 0)), Ray(Point(0.25, 0.75), Point(0.6, -0.8))]))
+    # test_accel.py:62-71 ray through a shared vertex
+    sc = Scene.from_geometry([Segment(Point(0.5, 0.5), Point(0.75, 0.85)),
+                              Segment(Point(0.5, 0.5), Point(0.75, 0.15))], normalize=False)
+    cases.append(("shared_vertex", sc, [Ray(Point(0.2, 0.5), Point(1, 0)),
+                                        Ray(Point(0.2, 0.5), Point(0.6, 0.8)),
+                                        Ray(Point(0.9, 0.5), Point(-1, 0))]))
+    # test_accel.py:31-37 tie at a joint (lowest id)
+    sc = Scene.from_geometry([Segment(Point(0.5, 0.5), Point(0.7, 0.8)),
+                              Segment(Point(0.5, 0.5), Point(0.7, 0.2))], normalize=False)
+    cases.append(("tie_lowest_id", sc, [Ray(Point(0.1, 0.5), Point(1, 0))]))
+    # polyline joint hit from the higher-id side + ray along an edge + collinear segment
+    sc = Scene.from_geometry([Segment(Point(0.3, 0.6), Point(0.5, 0.4)),
+                              Segment(Point(0.5, 0.4), Point(0.7, 0.6)),
+                              Segment(Point(0.2, 0.2), Point(0.8, 0.2)),
+                              Segment(Point(0.1, 0.85), Point(0.4, 0.85))], normalize=False)
+    cases.append(("joint_and_collinear", sc, [
+        Ray(Point(0.5, 0.05), Point(0, 1)),              # through the joint (0.5, 0.4)
+        Ray(Point(0.9, 0.4), Point(-1, 0)),              # horizontal through the joint
+        Ray(Point(0.05, 0.2), Point(1, 0)),              # collinear with segment 2
+        Ray(Point(0.95, 0.2), Point(-1, 0)),             # collinear, from the other side
+        Ray(Point(0.05, 0.85), Point(1, 0)),             # collinear with segment 3
+        Ray(Point(0.5, 0.5), Point(0, -1)),              # straight down onto the joint
+        Ray(Point(0.0, 0.0), Point(1, 1)),               # from the corner (box vertex)
+        Ray(Point(1.0, 0.5), Point(-1, 0)),              # from the boundary
+    ]))
+    # reference test scene (test_accel.py:47-59)
+    sc = random_segment_scene(25, seed=70)
+    cases.append(("random25", sc, sample_rays(sc, 1500, seed=1)))
+    # a refined mesh (Steiner + on-segment vertices, test_accel.py:74-81)
+    sc = random_segment_scene(15, seed=71)
+    cases.append(("refined15", sc, sample_rays(sc, 1500, seed=2)))
+
+    names = []
+    for name, sc, rays in cases:
+        tri = build_cdt(sc) if name != "refined15" else refine_cdt(build_cdt(sc), 20.0, 0.05)
+        tri = roundtrip(tri)
+        xy, kind = scene_arrays(sc)
+        vxy, v, nbr, flag = tri_arrays(tri)
+        r = ray_arr(rays)
+        walk = run_walk(tri, rays)
+        idx = SceneIndex(sc)
+        bf = [brute_force_closest(sc, ray, idx) for ray in rays]
+        d = dict(seg_xy=xy, seg_kind=kind, vxy=vxy, v=v, nbr=nbr, flag=flag, rays=r,
+                 bf_seg=np.array([-1 if h is None else h.seg for h in bf], np.int32),
+                 bf_t=np.array([np.nan if h is None else h.t for h in bf]))
+        d.update(prefixed("w_", walk))
+        # point location: brute vs anchor on origins, centroids and shared-edge midpoints
+        pts = [r_.origin for r_ in rays]
+        for tid in range(len(tri.tris)):
+            vv = tri.tris[tid].v
+            pts.append(Point(sum(tri.pos(k).x for k in vv) / 3, sum(tri.pos(k).y for k in vv) / 3))
+        for tid, i, a, b in tri.iter_edges():
+            pa, pb = tri.pos(a), tri.pos(b)
+            pts.append(Point((pa.x + pb.x) / 2, (pa.y + pb.y) / 2))
+        pts.extend(tri.pos(k) for k in range(len(tri.verts)))  # exact vertices (fan ties)
+        loc = TriLocator(tri)
+        d["loc_pts"] = np.array(pts, np.float64).reshape(-1, 2)
+        d["loc_anchor"] = np.array([loc.locate(p) for p in pts], np.int32)
+        d["loc_brute"] = np.array([locate_triangle(tri, p, "brute") for p in pts], np.int32)
+        out.update(prefixed(f"{name}__", d))
+        names.append(name)
+        print(f"known/{name}: {len(rays)} rays, {len(pts)} points", flush=True)
+    out["cases"] = np.array(names)
+
+    # geometry.py:136-166 against random cases (test_geometry.py:92-119 style)
+    rng = random.Random(42)
+    rs, ss, res = [], [], []
+    for _ in range(20000):
+        o = Point(rng.uniform(-1, 1), rng.uniform(-1, 1))
+        th = rng.uniform(0, 2 * math.pi)
+        ray = Ray(o, Point(math.cos(th), math.sin(th)))
+        a = Point(rng.uniform(-1, 1), rng.uniform(-1, 1))
+        b = Point(rng.uniform(-1, 1), rng.uniform(-1, 1))
+        if a == b:
+            continue
+        h = ray_segment_intersect(ray, Segment(a, b))
+        rs.append([ray.origin.x, ray.origin.y, ray.direction.x, ray.direction.y])
+        ss.append([a.x, a.y, b.x, b.y])
+        res.append([np.nan, np.nan] if h is None else [h[0], h[1]])
+    # degenerate: parallel / collinear (test_geometry.py:78-89)
+    for (ox, oy, dx, dy), (ax, ay, bx, by) in [((0, 0, 1, 0), (2, 0, 5, 0)), ((0, 0, 1, 0), (5, 0, 2, 0)),
+                                               ((0, 0, 1, 0), (-5, 0, -2, 0)), ((0, 0, 1, 0), (-1, 0, 3, 0)),
+                                               ((0, 0, 1, 0), (0.5, -1, 0.5, 1)), ((0, 0, 1, 0), (0.5, 1, 1.5, 1)),
+                                               ((0, 0, 0.6, 0.8), (0, 1, 1, 0))]:
+        ray = Ray(Point(ox, oy), Point(dx, dy))
+        h = ray_segment_intersect(ray, Segment(Point(ax, ay), Point(bx, by)))
+        rs.append([ray.origin.x, ray.origin.y, ray.direction.x, ray.direction.y])
+        ss.append([ax, ay, bx, by])
+        res.append([np.nan, np.nan] if h is None else [h[0], h[1]])
+    out["rsi_rays"] = np.array(rs, np.float64)
+    out["rsi_segs"] = np.array(ss, np.float64)
+    out["rsi_tu"] = np.array(res, np.float64)
+    np.savez_compressed(os.path.join(HERE, "known.npz"), **out)
+
+
+def make_hypot():
+    rng = np.random.default_rng(5)
+    n = 200000
+    x = rng.uniform(-1, 1, n) * 10.0 ** rng.uniform(-12, 2, n)
+    y = rng.uniform(-1, 1, n) * 10.0 ** rng.uniform(-12, 2, n)
+    y[:1000] = 0.0
+    x[1000:2000] = y[1000:2000]
+    h = np.array([math.hypot(a, b) for a, b in zip(x.tolist(), y.tolist())])
+    np.savez_compressed(os.path.join(HERE, "hypot.npz"), x=x, y=y, h=h)
+
+
+def make_config(cfg, nrays=4096):
+    d = os.path.join(FIX, cfg)
+    scene = Scene.load(os.path.join(d, "scene.txt"))
+    index = SceneIndex(scene)
+    box = BOXES.get(cfg, (0.0, 0.0, 1.0, 1.0))
+    out = {}
+    modes = [0, 1] if cfg in ("lines1024", "lines64") else [0]
+    for mode in modes:
+        arr = raygen(mode, box, 0, 0, nrays)
+        out[f"rays{mode}"] = arr
+        rays = rays_from(arr)
+        for which in ("cdt", "mwt"):
+            p = os.path.join(d, f"{which}.tri")
+            if not os.path.exists(p):
+                continue
+            tri = load_triangulation(p, scene)
+            w = run_walk(tri, rays, index=index)
+            out.update(prefixed(f"{which}{mode}_", w))
+            print(f"{cfg}/{which}/mode{mode}: steps {w['steps'].mean():.3f} hit {(w['seg'] >= 0).mean():.3f}",
+                  flush=True)
+        bf = [brute_force_closest(scene, r, index) for r in rays[:1024]]
+        out[f"bf{mode}_seg"] = np.array([-1 if h is None else h.seg for h in bf], np.int32)
+        out[f"bf{mode}_t"] = np.array([np.nan if h is None else h.t for h in bf])
+    np.savez_compressed(os.path.join(HERE, f"config_{cfg}.npz"), **out)
+
+
+def make_struct(cfg, nrays=1024):
+    from mintri.accel import C_T_GRID
+    d = os.path.join(FIX, cfg)
+    scene = Scene.load(os.path.join(d, "scene.txt"))
+    box = BOXES.get(cfg, (0.0, 0.0, 1.0, 1.0))
+    out = {}
+    for mode in (0, 1):
+        arr = raygen(mode, box, 0, 0, nrays)
+        out[f"rays{mode}"] = arr
+        rays = rays_from(arr)
+        grid = C_T_GRID if cfg == "lines1024" else (1.0,)
+        for c_t in grid:
+            bvh = build_bvh(scene, c_t)
+            kd = build_kdtree(scene, c_t)
+            rb = [bvh_intersect(bvh, r) for r in rays]
+            rk = []
+            for r in rays:
+                try:
+                    rk.append(kd_intersect(kd, r))
+                except TraversalError:
+                    rk.append((None, None))
+            tag = f"{mode}_ct{c_t:g}"
+            out[f"bvh{tag}_seg"] = np.array([-1 if h is None else h.seg for h, _ in rb], np.int32)
+            out[f"bvh{tag}_t"] = np.array([np.nan if h is None else h.t for h, _ in rb])
+            out[f"bvh{tag}_nodes"] = np.array([s.bvh_node_tests for _, s in rb], np.int32)
+            out[f"bvh{tag}_prims"] = np.array([s.bvh_prim_tests for _, s in rb], np.int32)
+            out[f"kd{tag}_seg"] = np.array([-1 if h is None else h.seg for h, _ in rk], np.int32)
+            out[f"kd{tag}_t"] = np.array([np.nan if h is None else h.t for h, _ in rk])
+            out[f"kd{tag}_nodes"] = np.array([-1 if s is None else s.kd_nodes_visited for _, s in rk], np.int32)
+            out[f"kd{tag}_ropes"] = np.array([-1 if s is None else s.kd_rope_steps for _, s in rk], np.int32)
+            out[f"kd{tag}_prims"] = np.array([-1 if s is None else s.kd_prim_tests for _, s in rk], np.int32)
+            print(f"struct {cfg} mode{mode} c_t={c_t}: bvh ops {np.mean(out[f'bvh{tag}_nodes'] + out[f'bvh{tag}_prims']):.2f}"
+                  f" kd ops {np.mean(out[f'kd{tag}_nodes'] + out[f'kd{tag}_ropes'] + out[f'kd{tag}_prims']):.2f}",
+                  flush=True)
+    np.savez_compressed(os.path.join(HERE, f"struct_{cfg}.npz"), **out)
+
+
+if __name__ == "__main__":
+    groups = sys.argv[1:] or ["known", "hypot"] + [f"config:{c}" for c in CONFIGS] + \
+        [f"struct:{c}" for c in CONFIGS[1:]]
+    for g in groups:
+        if g == "known":
+            make_known()
+        elif g == "hypot":
+            make_hypot()
+        elif g.startswith("config:"):
+            make_config(g.split(":", 1)[1])
+        elif g.startswith("struct:"):
+            make_struct(g.split(":", 1)[1])
+        else:
+            raise SystemExit(f"unknown group {g}")

@@ -1,0 +1,68 @@
+"""Parity of the CUDA engine against the C oracle (itself pinned to the
+reference by tests/test_oracle_golden.py) on the five BASELINE configs.
+
+Bar (BASELINE.json north_star): hit segment id, start triangle and step count
+bit-exact; hit distance t within 1e-12 relative (the engine is in fact
+bit-exact: no FMA contraction, reference operation order)."""
+import numpy as np
+import pytest
+
+from conftest import CONFIGS, box_of, fixture_paths
+
+pytestmark = pytest.mark.gpu
+
+T_RTOL = 1e-12
+
+
+def _mesh_pair(cfg, which):
+    paths = fixture_paths(cfg, which)
+    if paths is None:
+        pytest.skip(f"{cfg}/{which} fixture not generated")
+    from paper_2112_05570_b200.engine import DeviceMesh
+    from oracle import oracle as orc
+    return DeviceMesh.from_files(*paths), orc.Mesh.from_files(*paths)
+
+
+def _compare(got, ref, keys=("start", "seg", "steps", "status")):
+    ok_err = (ref["status"] & 1) == 0
+    for k in keys:
+        a, b = np.asarray(got[k]), np.asarray(ref[k])
+        if k == "steps":
+            a, b = a[ok_err], b[ok_err]
+        if k == "status":
+            a, b = a.view(np.uint32), b.view(np.uint32)
+        bad = np.nonzero(a != b)[0]
+        assert len(bad) == 0, f"{k}: {len(bad)} mismatches, first {bad[:5]} got {a[bad[:5]]} ref {b[bad[:5]]}"
+    hit = ref["seg"] >= 0
+    t_got, t_ref = got["t"][hit], ref["t"][hit]
+    rel = np.abs(t_got - t_ref) / np.maximum(1.0, np.abs(t_ref))
+    assert rel.max(initial=0.0) <= T_RTOL
+    assert np.all(np.isnan(got["t"][~hit]))
+
+
+@pytest.mark.parametrize("cfg", CONFIGS)
+@pytest.mark.parametrize("which", ["cdt", "mwt"])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_trace_with_device_locate(cfg, which, mode):
+    from oracle import oracle as orc
+    mesh, om = _mesh_pair(cfg, which)
+    n = 1 << 16
+    box = box_of(cfg)
+    rays_dev = mesh.raygen_device(mode, box, 0, 12345, n)
+    got = {k: v.cpu().numpy() for k, v in mesh.trace_device(rays_dev).items()}
+    rays = orc.raygen(mode, box, 0, 12345, n)
+    assert np.array_equal(rays_dev.cpu().numpy().view(np.uint64), rays.view(np.uint64))
+    ref = om.trace(rays)
+    _compare(got, ref)
+
+
+@pytest.mark.parametrize("cfg", CONFIGS)
+def test_trace_host_entry_point(cfg):
+    from oracle import oracle as orc
+    mesh, om = _mesh_pair(cfg, "mwt")
+    rays = orc.raygen(0, box_of(cfg), 7, 0, 20000)
+    ref = om.trace(rays)
+    got = mesh.trace(rays)
+    _compare(got, ref)
+    got2 = mesh.trace(rays, ref["start"])  # explicit start triangles
+    _compare(got2, ref)
