@@ -16,7 +16,7 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OUT_DIR = os.path.join(PKG, "_build")
 LIB = os.path.join(OUT_DIR, "libmwt.so")
-SOURCES = ["mwt_kernels.cu", "mwt_capi.cu", "mwt_pack.cpp"]
+SOURCES = ["mwt_walk.cu", "mwt_struct.cu", "mwt_capi.cu", "mwt_pack.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -37,7 +37,7 @@ def up_to_date() -> bool:
     if not os.path.exists(LIB):
         return False
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES + ["mwt_internal.h"]]
+    deps = [os.path.join(CSRC, s) for s in SOURCES + ["mwt_internal.h", "mwt_device.cuh"]]
     deps += [os.path.join(ROOT, "include", "mwt.h"), __file__]
     return all(os.path.getmtime(d) <= t for d in deps)
 

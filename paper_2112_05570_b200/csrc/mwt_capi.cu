@@ -87,6 +87,11 @@ extern "C" {
 
 int mwt_abi_version(void) { return MWT_ABI_VERSION; }
 
+int mwt_set_tuning(int refill_below, int min_blocks_per_sm) {
+    mwt::set_tuning(refill_below, min_blocks_per_sm);
+    return MWT_OK;
+}
+
 const char *mwt_last_error(void) { return g_err.c_str(); }
 
 int mwt_device_count(int *count) {
@@ -144,7 +149,7 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
         delete m;
         return cuda_fail(e, "mesh_create: upload");
     }
-    m->dev = mwt::MeshDev{P.nt, P.ns, P.res, link, cxy, lnbr, seg, kind, epr, epi, anc};
+    m->dev = mwt::MeshDev{P.nt, P.ns, P.res, P.flood_filter, link, cxy, lnbr, seg, kind, epr, epi, anc};
     m->info.num_vertices = P.nv;
     m->info.num_triangles = P.nt;
     m->info.num_segments = P.ns;

@@ -1,0 +1,299 @@
+#pragma once
+// Device helpers shared by the B200 (sm_100a) kernels of the ray-query engine.
+//
+//   K2 raygen      seeded isotropic rays (engine-defined, twin: oracle/raygen.py)
+//   K3 locate      TriLocator.locate            accel.py:219-330
+//   K4 walk        traverse_triangulation       accel.py:138-213
+//   K5 bvh         bvh_intersect                accel.py:460-518
+//   K6 kd          kd_intersect                 accel.py:712-832
+//   K7 histogram   per-ray results -> step / hit / status counters
+//   brute          brute_force_closest          accel.py:101-132
+//
+// Bit-exactness: CPython evaluates every + - * / in IEEE binary64 with no
+// fusion.  This translation unit is compiled with -fmad=false so no a*b+c is
+// contracted; fma() appears only where an EXACT product error term is wanted
+// (correctly rounded hypot).  Operation order follows the reference
+// expression by expression.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+#include "mwt_internal.h"
+
+namespace mwt {
+
+#define ST_ERROR MWT_ST_ERROR
+#define ST_FALLBACK MWT_ST_FALLBACK
+#define ST_GRAZING MWT_ST_GRAZING
+#define ST_CANON MWT_ST_CANON
+#define ST_PARALLEL MWT_ST_PARALLEL
+#define ST_ZERO_SIDE MWT_ST_ZERO_SIDE
+#define ST_MULTI MWT_ST_MULTI
+#define ST_LOC_TIE MWT_ST_LOC_TIE
+#define ST_LOC_BRUTE MWT_ST_LOC_BRUTE
+#define ST_LOC_OUTSIDE MWT_ST_LOC_OUTSIDE
+#define ST_OVERFLOW MWT_ST_OVERFLOW
+
+constexpr int kThreads = 256;
+constexpr int kFloodCap = 32;
+constexpr int kBvhStack = 128;
+constexpr int kKdMailbox = 512;
+
+struct Ray {
+    double ox, oy, dx, dy;
+};
+
+// 32-B read-only load as two 16-B vector loads (no __ldg overload for double4)
+__device__ __forceinline__ double4 ldg4d(const double4 *p) {
+    const double2 *q = reinterpret_cast<const double2 *>(p);
+    double2 a = __ldg(q), b = __ldg(q + 1);
+    return make_double4(a.x, a.y, b.x, b.y);
+}
+
+// ---------------------------------------------------------------------------
+// correctly rounded hypot (CPython's math.hypot is correctly rounded; the
+// CUDA libm hypot is not).  Fast filtered decision; exact expansion fallback.
+
+__device__ __forceinline__ void two_sum(double a, double b, double &s, double &e) {
+    double x = a + b;
+    double bv = x - a;
+    double av = x - bv;
+    s = x;
+    e = (a - av) + (b - bv);
+}
+
+static __device__ __noinline__ int exact_sign8(const double *v) {
+    double h[16];
+    int m = 0;
+    for (int k = 0; k < 8; k++) {
+        double q = v[k];
+        int mm = 0;
+        for (int i = 0; i < m; i++) {
+            double s, e;
+            two_sum(q, h[i], s, e);
+            if (e != 0.0) h[mm++] = e;
+            q = s;
+        }
+        if (q != 0.0) h[mm++] = q;
+        m = mm;
+    }
+    if (m == 0) return 0;
+    return h[m - 1] > 0.0 ? 1 : -1;
+}
+
+// sign of (x^2 + y^2) - (c + d)^2, d = +-2^k
+static __device__ __noinline__ int cmp_mid_exact(double x, double y, double c, double d) {
+    double v[8];
+    double sh = x * x, th = y * y, ph = c * c;
+    v[0] = sh;
+    v[1] = fma(x, x, -sh);
+    v[2] = th;
+    v[3] = fma(y, y, -th);
+    v[4] = -ph;
+    v[5] = -fma(c, c, -ph);
+    v[6] = -(2.0 * c * d);
+    v[7] = -(d * d);
+    return exact_sign8(v);
+}
+
+static __device__ __noinline__ double cr_hypot(double x, double y) {
+    x = fabs(x);
+    y = fabs(y);
+    if (isinf(x) || isinf(y)) return CUDART_INF;
+    if (isnan(x) || isnan(y)) return CUDART_NAN;
+    if (x < y) {
+        double t = x;
+        x = y;
+        y = t;
+    }
+    if (y == 0.0) return x;
+    double scale = 1.0;
+    if (x > 0x1p+500) {
+        x *= 0x1p-600; y *= 0x1p-600; scale = 0x1p+600;
+    } else if (x < 0x1p-500) {
+        x *= 0x1p+600; y *= 0x1p+600; scale = 0x1p-600;
+    }
+    double sh = x * x, sl = fma(x, x, -sh);
+    double th = y * y, tl = fma(y, y, -th);
+    double S, es;
+    two_sum(sh, th, S, es);
+    double c = sqrt(S);
+    for (int it = 0; it < 4; it++) {
+        double ph = c * c, pl = fma(c, c, -ph);
+        double d1 = S - ph;  // exact: c*c within a few ulp of S (Sterbenz)
+        double delta = d1 + (((es + sl) + tl) - pl);  // ~ (x^2+y^2) - c^2
+        double up = nextafter(c, CUDART_INF), dn = nextafter(c, 0.0);
+        double hu = 0.5 * (up - c), hd = 0.5 * (c - dn);
+        double Tu = 2.0 * c * hu + hu * hu;  // (c+hu)^2 - c^2
+        double Td = 2.0 * c * hd - hd * hd;  // c^2 - (c-hd)^2
+        double margin = 0x1p-40 * Tu;
+        if (delta > Tu + margin) { c = up; continue; }
+        if (delta < -Td - margin) { c = dn; continue; }
+        if (fabs(delta - Tu) <= margin || fabs(delta + Td) <= margin) {
+            int su = cmp_mid_exact(x, y, c, hu);
+            if (su > 0) { c = up; continue; }
+            int sd = cmp_mid_exact(x, y, c, -hd);
+            if (sd < 0) { c = dn; continue; }
+            unsigned long long b = (unsigned long long)__double_as_longlong(c);
+            if (su == 0 && (b & 1ull)) c = up;
+            else if (sd == 0 && (b & 1ull)) c = dn;
+        }
+        break;
+    }
+    return c * scale;
+}
+
+// ---------------------------------------------------------------------------
+// K2: ray generator (twin: oracle/raygen.py, oracle/mwt_oracle.c orc_raygen)
+
+constexpr unsigned long long kGolden = 0x9E3779B97F4A7C15ull;
+
+__host__ __device__ __forceinline__ unsigned long long mix64(unsigned long long z) {
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+static inline unsigned long long ray_key(unsigned long long seed, unsigned long long stream) {
+    return mix64(mix64(seed + kGolden) ^ (stream * 0xD1B54A32D192ED03ull));
+}
+
+__device__ __forceinline__ double u01(unsigned long long s0, unsigned long long k) {
+    return (double)(mix64(s0 + (k + 1ull) * kGolden) >> 11) * 0x1p-53;
+}
+
+struct Box {
+    double x0, y0, x1, y1;
+};
+
+__device__ __forceinline__ Ray gen_ray(int mode, const Box &b, unsigned long long key,
+                                       unsigned long long idx) {
+    unsigned long long s0 = mix64(key ^ idx);
+    double x = 1.0, y = 0.0, r2 = 1.0;
+    bool ok = false;
+    for (int a = 0; a < 64; a++) {
+        x = 2.0 * u01(s0, 2 * a) - 1.0;
+        y = 2.0 * u01(s0, 2 * a + 1) - 1.0;
+        r2 = x * x + y * y;
+        if (r2 <= 1.0 && r2 > 0x1p-60) { ok = true; break; }
+    }
+    Ray r;
+    r.dx = 1.0;
+    r.dy = 0.0;
+    if (ok) {
+        double n = sqrt(r2);
+        r.dx = x / n;
+        r.dy = y / n;
+    }
+    double W = b.x1 - b.x0, H = b.y1 - b.y0;
+    if (mode == MWT_RAYS_INTERIOR) {
+        r.ox = b.x0 + W * u01(s0, 128);
+        r.oy = b.y0 + H * u01(s0, 129);
+    } else {
+        double cx = b.x0 + 0.5 * W, cy = b.y0 + 0.5 * H;
+        double nx = -r.dy, ny = r.dx;
+        double w = 0.5 * (fabs(nx) * W + fabs(ny) * H);
+        double s = w * (2.0 * u01(s0, 128) - 1.0);
+        double px = cx + s * nx, py = cy + s * ny;
+        double tx = -CUDART_INF, ty = -CUDART_INF;
+        if (r.dx > 0.0) tx = (b.x0 - px) / r.dx;
+        else if (r.dx < 0.0) tx = (b.x1 - px) / r.dx;
+        if (r.dy > 0.0) ty = (b.y0 - py) / r.dy;
+        else if (r.dy < 0.0) ty = (b.y1 - py) / r.dy;
+        if (tx >= ty) {
+            r.ox = r.dx > 0.0 ? b.x0 : b.x1;
+            double oy = py + tx * r.dy;
+            r.oy = oy < b.y0 ? b.y0 : (oy > b.y1 ? b.y1 : oy);
+        } else {
+            r.oy = r.dy > 0.0 ? b.y0 : b.y1;
+            double ox = px + ty * r.dx;
+            r.ox = ox < b.x0 ? b.x0 : (ox > b.x1 ? b.x1 : ox);
+        }
+    }
+    return r;
+}
+
+// ---------------------------------------------------------------------------
+// geometry (geometry.py)
+
+__device__ __forceinline__ double sa2(double2 a, double2 b, double px, double py) {
+    // geometry.py:81-83 signed_area2(a, b, p)
+    return (b.x - a.x) * (py - a.y) - (b.y - a.y) * (px - a.x);
+}
+
+__device__ __forceinline__ double side_of(const Ray &r, double2 v) {
+    // accel.py:157
+    return r.dx * (v.y - r.oy) - r.dy * (v.x - r.ox);
+}
+
+// geometry.py:136-166
+__device__ __forceinline__ bool rsi(const Ray &r, double4 s, double &t, double &u, bool &par) {
+    double ex = s.z - s.x, ey = s.w - s.y;
+    double denom = r.dx * ey - r.dy * ex;
+    double wx = s.x - r.ox, wy = s.y - r.oy;
+    if (denom == 0.0) {
+        par = true;
+        if (wx * r.dy - wy * r.dx != 0.0) return false;
+        double ta = wx * r.dx + wy * r.dy;
+        double tb = (s.z - r.ox) * r.dx + (s.w - r.oy) * r.dy;
+        if (ta < 0.0 && tb < 0.0) return false;
+        if (ta < 0.0) { t = tb; u = 1.0; return true; }
+        if (tb < 0.0) { t = ta; u = 0.0; return true; }
+        if (ta <= tb) { t = ta; u = 0.0; } else { t = tb; u = 1.0; }
+        return true;
+    }
+    double tt = (wx * ey - wy * ex) / denom;
+    double uu = (wx * r.dy - wy * r.dx) / denom;
+    if (tt < 0.0 || uu < 0.0 || uu > 1.0) return false;
+    t = tt;
+    u = uu;
+    return true;
+}
+
+// accel.py:82-98 SceneIndex.canonical
+__device__ __forceinline__ int canonical(const MeshDev &M, const Ray &r, int sid, double t, double u, double &ot,
+                         double &ou) {
+    int best = sid;
+    double bt = t, bu = u;
+    if (u <= 1e-9 || u >= 1.0 - 1e-9) {
+        int e = 2 * sid + (u <= 1e-9 ? 0 : 1);
+        int2 rg = __ldg(M.ep_range + e);
+        double at = fabs(t);
+        double tol = 1e-9 * (at > 1.0 ? at : 1.0);
+        for (int k = 0; k < rg.y; k++) {
+            int sid2 = __ldg(M.ep_ids + rg.x + k);
+            if (sid2 >= best) continue;
+            double t2, u2;
+            bool par = false;
+            if (!rsi(r, ldg4d(M.seg + sid2), t2, u2, par)) continue;
+            if (fabs(t2 - t) <= tol) {
+                best = sid2;
+                bt = t2;
+                bu = u2;
+            }
+        }
+    }
+    ot = bt;
+    ou = bu;
+    return best;
+}
+
+__device__ __forceinline__ uint32_t pick(int4 L, int i) {
+    return (uint32_t)(i == 0 ? L.x : (i == 1 ? L.y : L.z));
+}
+
+__device__ __forceinline__ Ray load_ray(const double *rays, long long i) {
+    const double2 *p = reinterpret_cast<const double2 *>(rays) + 2 * i;
+    double2 a = __ldg(p), b = __ldg(p + 1);
+    Ray r;
+    r.ox = a.x;
+    r.oy = a.y;
+    r.dx = b.x;
+    r.dy = b.y;
+    return r;
+}
+
+int grid_for(long long n);
+
+}  // namespace mwt

@@ -33,7 +33,8 @@ namespace mwt {
 //   ep_range[2S] int2 (offset, count) into ep_ids: for endpoint e of
 //                   segment s (2s = a, 2s+1 = b), the ascending geometry
 //                   segment ids sharing that exact point (SceneIndex.endpoint_map).
-//   anchor[res*res] int32 TriLocator anchor triangles, row-major (cy, cx).
+//   anchor[res*res] int32 seed grid over [0,1]^2: triangle holding each cell
+//                   centre (Triangulation.locate, trimesh.py:386-416), row-major.
 //
 // One walk step reads link[N] (16 B) + cxy[3N+j] (16 B) = 32 algorithmic B.
 // ---------------------------------------------------------------------------
@@ -45,7 +46,7 @@ constexpr uint32_t kSidMask = 0x3FFFFFFFu;
 
 struct HostPacked {
     int32_t nv = 0, nt = 0, ns = 0;
-    int32_t res = 0, anchors_not_strict = 0;
+    int32_t res = 0, anchors_not_strict = 0, flood_filter = 1;
     std::vector<int32_t> link;      // 4*nt
     std::vector<double> cxy;        // 6*nt
     std::vector<int32_t> lnbr;      // 4*nt
@@ -64,7 +65,7 @@ int pack_mesh(const double *vx, const double *vy, int32_t nverts, const int32_t 
 
 // Device view passed by value to kernels.
 struct MeshDev {
-    int32_t nt, ns, res;
+    int32_t nt, ns, res, flood_filter;
     const int4 *link;
     const double2 *cxy;
     const int4 *lnbr;
@@ -106,6 +107,7 @@ int launch_trace(const MeshDev &m, const double *rays, const int32_t *start, int
 int launch_trace_generated(const MeshDev &m, int mode, const double *box, uint64_t seed,
                            uint64_t first, int64_t n, int32_t *o_seg, double *o_t,
                            int32_t *o_steps, long long *hist, void *stream);
+void set_tuning(int refill_below, int min_blocks);
 int launch_histogram(const int32_t *seg, const int32_t *steps, const uint32_t *st, int64_t n,
                      long long *hist, void *stream);
 int launch_bvh(const MeshDev &m, const BvhDev &b, const double *rays, int64_t n, int32_t *o_seg,

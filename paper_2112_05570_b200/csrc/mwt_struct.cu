@@ -1,0 +1,297 @@
+// K5 BVH, K6 roped kd-tree and brute-force kernels (B200, sm_100a).
+// Compiled with -fmad=false: reference operation order, no contraction.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+#include "mwt_device.cuh"
+
+namespace mwt {
+
+// ---------------------------------------------------------------------------
+// K5: BVH, accel.py:460-518
+
+__device__ __forceinline__ bool ray_box(const Ray &r, double4 b, double &tn) {
+    double tmin = 0.0, tmax = CUDART_INF;
+    // x slab then y slab; Python max/min keep the first operand on ties
+    if (r.dx == 0.0) {
+        if (r.ox < b.x || r.ox > b.z) return false;
+    } else {
+        double t1 = (b.x - r.ox) / r.dx, t2 = (b.z - r.ox) / r.dx;
+        if (t1 > t2) { double s = t1; t1 = t2; t2 = s; }
+        tmin = t1 > tmin ? t1 : tmin;
+        tmax = t2 < tmax ? t2 : tmax;
+        if (tmin > tmax) return false;
+    }
+    if (r.dy == 0.0) {
+        if (r.oy < b.y || r.oy > b.w) return false;
+    } else {
+        double t1 = (b.y - r.oy) / r.dy, t2 = (b.w - r.oy) / r.dy;
+        if (t1 > t2) { double s = t1; t1 = t2; t2 = s; }
+        tmin = t1 > tmin ? t1 : tmin;
+        tmax = t2 < tmax ? t2 : tmax;
+        if (tmin > tmax) return false;
+    }
+    tn = tmin;
+    return true;
+}
+
+__global__ void __launch_bounds__(kThreads) k_bvh(MeshDev M, BvhDev B, const double *rays,
+                                                  long long n, int32_t *o_seg, double *o_t,
+                                                  double *o_u, int32_t *o_nodes, int32_t *o_prims,
+                                                  uint32_t *o_st) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        Ray r = load_ray(rays, i);
+        int nodes = 1, prims = 0, bsid = -1;
+        bool have = false;
+        uint32_t st = 0;
+        double bt = 0.0, bu = 0.0, tn;
+        int seg = -1;
+        double ot = CUDART_NAN, ou = CUDART_NAN;
+        if (ray_box(r, ldg4d(B.box), tn)) {
+            double st_t[kBvhStack];
+            int st_n[kBvhStack];
+            int top = 0;
+            st_t[0] = tn;
+            st_n[0] = 0;
+            top = 1;
+            while (top > 0) {
+                top--;
+                double tnear = st_t[top];
+                int node = st_n[top];
+                if (have && tnear > bt + 1e-12) continue;
+                int2 ch = __ldg(B.child + node);
+                if (ch.x < 0) {
+                    int2 pr = __ldg(B.prange + node);
+                    for (int k = 0; k < pr.y; k++) {
+                        int sid = __ldg(B.prims + pr.x + k);
+                        prims++;
+                        double t, u;
+                        bool par = false;
+                        if (!rsi(r, ldg4d(M.seg + sid), t, u, par)) continue;
+                        if (!have || t < bt) { have = true; bt = t; bsid = sid; bu = u; }
+                    }
+                    continue;
+                }
+                double tl = 0.0, tr = 0.0;
+                nodes += 2;
+                bool hl = ray_box(r, ldg4d(B.box + ch.x), tl) && (!have || tl <= bt + 1e-12);
+                bool hr = ray_box(r, ldg4d(B.box + ch.y), tr) && (!have || tr <= bt + 1e-12);
+                if (top + 2 > kBvhStack) { st |= ST_OVERFLOW; break; }
+                // children sorted by tnear descending (stable) then pushed: the
+                // nearer pops first; on equal tnear the right child pops first
+                if (hl && hr) {
+                    if (tr > tl) {
+                        st_t[top] = tr; st_n[top] = ch.y; top++;
+                        st_t[top] = tl; st_n[top] = ch.x; top++;
+                    } else {
+                        st_t[top] = tl; st_n[top] = ch.x; top++;
+                        st_t[top] = tr; st_n[top] = ch.y; top++;
+                    }
+                } else if (hl) {
+                    st_t[top] = tl; st_n[top] = ch.x; top++;
+                } else if (hr) {
+                    st_t[top] = tr; st_n[top] = ch.y; top++;
+                }
+            }
+            if (have) seg = canonical(M, r, bsid, bt, bu, ot, ou);
+        }
+        if (o_seg) o_seg[i] = seg;
+        if (o_t) o_t[i] = ot;
+        if (o_u) o_u[i] = ou;
+        if (o_nodes) o_nodes[i] = nodes;
+        if (o_prims) o_prims[i] = prims;
+        if (o_st) o_st[i] = st;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K6: roped kd-tree, accel.py:712-832
+
+__device__ __forceinline__ int kd_descend(const KdDev &K, int node, double px, double py, double dx,
+                                          double dy, int &nodes, bool count) {
+    int a;
+    while ((a = __ldg(K.axis + node)) >= 0) {
+        if (count) nodes++;
+        double coord = a == 0 ? px : py;
+        double pos = __ldg(K.pos + node);
+        int2 ch = __ldg(K.child + node);
+        if (coord < pos) node = ch.x;
+        else if (coord > pos) node = ch.y;
+        else {
+            double d = a == 0 ? dx : dy;
+            node = d > 0.0 ? ch.y : ch.x;
+        }
+    }
+    return node;
+}
+
+__global__ void __launch_bounds__(kThreads) k_kd(MeshDev M, KdDev K, const double *rays,
+                                                 long long n, int32_t *o_seg, double *o_t,
+                                                 double *o_u, int32_t *o_nodes, int32_t *o_ropes,
+                                                 int32_t *o_prims, uint32_t *o_st) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        Ray r = load_ray(rays, i);
+        int nodes = 0, ropes = 0, prims = 0, bsid = -1, seg = -1;
+        bool have = false, done = false;
+        uint32_t st = 0;
+        double bt = 0.0, bu = 0.0, ot = CUDART_NAN, ou = CUDART_NAN;
+        int tested[kKdMailbox];
+        int ntested = 0;
+        int dummy = 0;
+        int cur = kd_descend(K, 0, r.ox, r.oy, r.dx, r.dy, dummy, false);  // locate_leaf
+        long long guard = 4LL * K.nleaves + 16;
+        while (guard > 0 && !done) {
+            guard--;
+            nodes++;
+            double4 bb = ldg4d(K.box + cur);
+            double t_exit = CUDART_INF;
+            int side = -1;
+            if (r.dx > 0.0) {
+                double tx = (bb.z - r.ox) / r.dx;
+                if (tx < t_exit) { t_exit = tx; side = 1; }
+            } else if (r.dx < 0.0) {
+                double tx = (bb.x - r.ox) / r.dx;
+                if (tx < t_exit) { t_exit = tx; side = 0; }
+            }
+            if (r.dy > 0.0) {
+                double ty = (bb.w - r.oy) / r.dy;
+                if (ty < t_exit) { t_exit = ty; side = 3; }
+            } else if (r.dy < 0.0) {
+                double ty = (bb.y - r.oy) / r.dy;
+                if (ty < t_exit) { t_exit = ty; side = 2; }
+            }
+            int2 pr = __ldg(K.prange + cur);
+            for (int k = 0; k < pr.y; k++) {
+                int sid = __ldg(K.prims + pr.x + k);
+                bool dup = false;
+                for (int q = 0; q < ntested; q++) dup |= (tested[q] == sid);
+                if (dup) continue;
+                if (ntested == kKdMailbox) { st |= ST_OVERFLOW; done = true; break; }
+                tested[ntested++] = sid;
+                prims++;
+                double t, u;
+                bool par = false;
+                if (!rsi(r, ldg4d(M.seg + sid), t, u, par)) continue;
+                if (!have || t < bt) { have = true; bt = t; bsid = sid; bu = u; }
+            }
+            if (done) break;
+            if (have && bt <= t_exit + 1e-12) {
+                seg = canonical(M, r, bsid, bt, bu, ot, ou);
+                done = true;
+                break;
+            }
+            if (side < 0) { done = true; break; }
+            int rope = ((const int *)(K.ropes + cur))[side];
+            if (rope < 0) { done = true; break; }
+            ropes += ((const int *)(K.rope_cost + cur))[side];
+            double px = r.ox + t_exit * r.dx, py = r.oy + t_exit * r.dy;
+            cur = kd_descend(K, rope, px, py, r.dx, r.dy, nodes, true);
+        }
+        if (!done) st |= ST_ERROR;
+        if (o_seg) o_seg[i] = seg;
+        if (o_t) o_t[i] = ot;
+        if (o_u) o_u[i] = ou;
+        if (o_nodes) o_nodes[i] = nodes;
+        if (o_ropes) o_ropes[i] = ropes;
+        if (o_prims) o_prims[i] = prims;
+        if (o_st) o_st[i] = st;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// brute force, accel.py:101-132
+
+__global__ void __launch_bounds__(kThreads) k_brute(MeshDev M, const double *rays, long long n,
+                                                    int32_t *o_seg, double *o_t, double *o_u) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        Ray r = load_ray(rays, i);
+        bool have = false;
+        int bsid = -1;
+        double bt = 0.0, bu = 0.0;
+        for (int s = 0; s < M.ns; s++) {
+            if (__ldg(M.segkind + s) != 0) continue;
+            double4 S = ldg4d(M.seg + s);
+            double ex = S.z - S.x, ey = S.w - S.y;
+            double wx = S.x - r.ox, wy = S.y - r.oy;
+            double denom = r.dx * ey - r.dy * ex;
+            if (denom == 0.0) continue;
+            double t = (wx * ey - wy * ex) / denom;
+            double u = (wx * r.dy - wy * r.dx) / denom;
+            if (t >= 0.0 && u >= 0.0 && u <= 1.0 && (!have || t < bt)) {
+                have = true; bt = t; bsid = s; bu = u;
+            }
+        }
+        for (int s = 0; s < M.ns; s++) {  // collinear fallback
+            if (__ldg(M.segkind + s) != 0) continue;
+            double4 S = ldg4d(M.seg + s);
+            double ex = S.z - S.x, ey = S.w - S.y;
+            double wx = S.x - r.ox, wy = S.y - r.oy;
+            double denom = r.dx * ey - r.dy * ex;
+            if (!(denom == 0.0 && wx * r.dy - wy * r.dx == 0.0)) continue;
+            double t, u;
+            bool par = false;
+            if (rsi(r, S, t, u, par) && (!have || t < bt)) {
+                have = true; bt = t; bsid = s; bu = u;
+            }
+        }
+        int seg = -1;
+        double ot = CUDART_NAN, ou = CUDART_NAN;
+        if (have) seg = canonical(M, r, bsid, bt, bu, ot, ou);
+        if (o_seg) o_seg[i] = seg;
+        if (o_t) o_t[i] = ot;
+        if (o_u) o_u[i] = ou;
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// launchers
+
+#define MWT_LAUNCH_RET return (int)cudaGetLastError()
+
+int grid_for(long long n) {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    long long blocks = (n + kThreads - 1) / kThreads;
+    long long cap = (long long)sms * 8;  // 8 resident 256-thread CTAs per SM
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    return (int)blocks;
+}
+
+int launch_bvh(const MeshDev &m, const BvhDev &b, const double *rays, int64_t n, int32_t *o_seg,
+               double *o_t, double *o_u, int32_t *o_nodes, int32_t *o_prims, uint32_t *o_st,
+               void *stream) {
+    if (n <= 0) return 0;
+    k_bvh<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(m, b, rays, n, o_seg, o_t, o_u,
+                                                              o_nodes, o_prims, o_st);
+    MWT_LAUNCH_RET;
+}
+
+int launch_kd(const MeshDev &m, const KdDev &k, const double *rays, int64_t n, int32_t *o_seg,
+              double *o_t, double *o_u, int32_t *o_nodes, int32_t *o_ropes, int32_t *o_prims,
+              uint32_t *o_st, void *stream) {
+    if (n <= 0) return 0;
+    k_kd<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(m, k, rays, n, o_seg, o_t, o_u,
+                                                             o_nodes, o_ropes, o_prims, o_st);
+    MWT_LAUNCH_RET;
+}
+
+int launch_brute(const MeshDev &m, const double *rays, int64_t n, int32_t *o_seg, double *o_t,
+                 double *o_u, void *stream) {
+    if (n <= 0) return 0;
+    k_brute<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(m, rays, n, o_seg, o_t, o_u);
+    MWT_LAUNCH_RET;
+}
+
+}  // namespace mwt

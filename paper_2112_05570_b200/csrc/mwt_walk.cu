@@ -1,0 +1,718 @@
+// K2 ray generation, K3 point location, K4 the MWT walk and K7 histograms
+// for B200 (sm_100a).  Compiled with -fmad=false: every fp64 expression is
+// evaluated in the reference's operation order with no contraction.
+//
+// Execution model (K4): persistent warps.  Each warp owns a contiguous chunk
+// of ray indices; a lane whose ray has terminated goes idle, and once at most
+// `refill_below` lanes of the warp are still walking, all idle lanes fetch the
+// next rays of the chunk together (ballot + popc rank), generate / load them,
+// locate their start triangle and enter the walk.  Walk steps therefore run
+// with most lanes busy, and the expensive per-ray prologue (raygen + locate)
+// runs with many lanes at once.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+#include "mwt_device.cuh"
+
+namespace mwt {
+
+// ---------------------------------------------------------------------------
+// K3: point location.  Result = TriLocator.locate (accel.py:284-289): the
+// lowest id among the neighbour-connected triangles that _contains p
+// (accel.py:219-238).  Any containing triangle seeds the same flood, so the
+// seed search here is the engine's own: a fine grid of cell-centre triangles
+// (packer) and a straight walk toward p with the reference's exit rule
+// (accel.py:314-322, direction left unnormalised), brute-force scan on
+// failure (accel.py:287-288).
+
+__device__ __forceinline__ void corners(const MeshDev &M, int t, double2 &P0, double2 &P1,
+                                        double2 &P2) {
+    P0 = __ldg(M.cxy + 3 * t);
+    P1 = __ldg(M.cxy + 3 * t + 1);
+    P2 = __ldg(M.cxy + 3 * t + 2);
+}
+
+// accel.py:219-223 with geometry.py:81-83 per edge i: signed_area2(P[i+1], P[i+2], p)
+__device__ __forceinline__ void edge_areas(double2 P0, double2 P1, double2 P2, double px, double py,
+                                           double &e0, double &e1, double &e2) {
+    e0 = sa2(P1, P2, px, py);
+    e1 = sa2(P2, P0, px, py);
+    e2 = sa2(P0, P1, px, py);
+}
+
+__device__ __forceinline__ bool inside(double e0, double e1, double e2) {
+    return e0 >= -1e-15 && e1 >= -1e-15 && e2 >= -1e-15;
+}
+
+__device__ __forceinline__ bool contains_t(const MeshDev &M, int t, double px, double py) {
+    double2 P0, P1, P2;
+    corners(M, t, P0, P1, P2);
+    double e0, e1, e2;
+    edge_areas(P0, P1, P2, px, py, e0, e1, e2);
+    return inside(e0, e1, e2);
+}
+
+// locate_brute_force, accel.py:241-253.  Cold path: arguments by value so no
+// caller state becomes address-taken.
+struct LocRes {
+    int tid;
+    uint32_t st;
+};
+
+__device__ __noinline__ LocRes loc_brute(const double2 *cxy, int nt, double px, double py) {
+    for (int t = 0; t < nt; t++) {
+        double2 P0 = __ldg(cxy + 3 * t), P1 = __ldg(cxy + 3 * t + 1), P2 = __ldg(cxy + 3 * t + 2);
+        double e0, e1, e2;
+        e0 = sa2(P1, P2, px, py);
+        e1 = sa2(P2, P0, px, py);
+        e2 = sa2(P0, P1, px, py);
+        if (e0 >= -1e-15 && e1 >= -1e-15 && e2 >= -1e-15) return LocRes{t, 0u};
+    }
+    int best = 0;
+    double bd = CUDART_INF;
+    for (int t = 0; t < nt; t++) {
+        double2 P0 = __ldg(cxy + 3 * t), P1 = __ldg(cxy + 3 * t + 1), P2 = __ldg(cxy + 3 * t + 2);
+        double cx = ((P0.x + P1.x) + P2.x) / 3.0;
+        double cy = ((P0.y + P1.y) + P2.y) / 3.0;
+        double d = cr_hypot(cx - px, cy - py);
+        if (d < bd) {
+            bd = d;
+            best = t;
+        }
+    }
+    return LocRes{best, (uint32_t)ST_LOC_OUTSIDE};
+}
+
+// _resolve_tie, accel.py:226-238, general case (some edge value <= 1e-12):
+// min tid over the flood of neighbour triangles containing p.  A neighbour
+// across edge i can contain p only if this triangle's value for edge i is
+// <= ~1e-14 (both are roundings of one exact quantity of opposite sign), so
+// larger values skip the exact test without changing the result.
+__device__ __noinline__ LocRes flood(const double2 *cxy, const int4 *lnbr, int filter, int tid,
+                                    double px, double py) {
+    int seen[kFloodCap];
+    int stack[kFloodCap];
+    int nseen = 1, top = 1, best = tid;
+    seen[0] = tid;
+    stack[0] = tid;
+    const bool filt = filter && fabs(px) <= 4.0 && fabs(py) <= 4.0;
+    while (top > 0) {
+        int cur = stack[--top];
+        if (cur < best) best = cur;
+        double2 P0 = __ldg(cxy + 3 * cur), P1 = __ldg(cxy + 3 * cur + 1), P2 = __ldg(cxy + 3 * cur + 2);
+        double e[3];
+        e[0] = sa2(P1, P2, px, py);
+        e[1] = sa2(P2, P0, px, py);
+        e[2] = sa2(P0, P1, px, py);
+        int4 NB = __ldg(lnbr + cur);
+        for (int i = 0; i < 3; i++) {
+            int word = (int)pick(NB, i);
+            if (word < 0) continue;
+            if (filt && e[i] > 1e-12) continue;
+            int nb = word >> 2;
+            bool dup = false;
+            for (int k = 0; k < nseen; k++) dup |= (seen[k] == nb);
+            if (dup) continue;
+            double2 Q0 = __ldg(cxy + 3 * nb), Q1 = __ldg(cxy + 3 * nb + 1), Q2 = __ldg(cxy + 3 * nb + 2);
+            if (!(sa2(Q1, Q2, px, py) >= -1e-15 && sa2(Q2, Q0, px, py) >= -1e-15 &&
+                  sa2(Q0, Q1, px, py) >= -1e-15))
+                continue;
+            if (nseen == kFloodCap) return LocRes{best, (uint32_t)ST_OVERFLOW};
+            seen[nseen++] = nb;
+            stack[top++] = nb;
+        }
+    }
+    return LocRes{best, nseen > 1 ? (uint32_t)ST_LOC_TIE : 0u};
+}
+
+// returns the start triangle and its corners
+__device__ __forceinline__ int locate(const MeshDev &M, double px, double py, uint32_t &st,
+                                      double2 &P0, double2 &P1, double2 &P2) {
+    const int res = M.res;
+    const double dres = (double)res;
+    double vx = px * dres, vy = py * dres;
+    int cx = vx < 0.0 ? 0 : (vx >= dres ? res - 1 : (int)vx);
+    int cy = vy < 0.0 ? 0 : (vy >= dres ? res - 1 : (int)vy);
+    if (!(vx == vx)) cx = 0;
+    if (!(vy == vy)) cy = 0;
+    const double sx = ((double)cx + 0.5) / dres, sy = ((double)cy + 0.5) / dres;
+    const double dx = px - sx, dy = py - sy;
+    int cur = __ldg(M.anchor + cy * res + cx);
+    int ent = -1;
+    double e0, e1, e2;
+    bool found = false;
+    const int cap = 4 * M.nt + 16;
+    for (int it = 0; it < cap; it++) {
+        corners(M, cur, P0, P1, P2);
+        edge_areas(P0, P1, P2, px, py, e0, e1, e2);
+        if (inside(e0, e1, e2)) {
+            found = true;
+            break;
+        }
+        // straight walk toward p, exit rule of accel.py:314-322
+        double s0 = dx * (P0.y - sy) - dy * (P0.x - sx);
+        double s1 = dx * (P1.y - sy) - dy * (P1.x - sx);
+        double s2 = dx * (P2.y - sy) - dy * (P2.x - sx);
+        int best = -1;
+        double bt = 0.0;
+        if (ent != 0 && s1 <= 0.0 && 0.0 <= s2 && s2 - s1 > bt) { bt = s2 - s1; best = 0; }
+        if (ent != 1 && s2 <= 0.0 && 0.0 <= s0 && s0 - s2 > bt) { bt = s0 - s2; best = 1; }
+        if (ent != 2 && s0 <= 0.0 && 0.0 <= s1 && s1 - s0 > bt) { bt = s1 - s0; best = 2; }
+        if (best < 0) break;
+        int word = (int)pick(__ldg(M.lnbr + cur), best);
+        if (word < 0) break;
+        cur = word >> 2;
+        ent = word & 3;
+    }
+    if (!found) {
+        const LocRes lr = loc_brute(M.cxy, M.nt, px, py);
+        st |= ST_LOC_BRUTE | lr.st;
+        cur = lr.tid;
+        corners(M, cur, P0, P1, P2);
+        edge_areas(P0, P1, P2, px, py, e0, e1, e2);
+    }
+    if (M.flood_filter && fabs(px) <= 4.0 && fabs(py) <= 4.0) {
+        // only neighbours across edges with value <= 1e-12 can contain p; a
+        // point strictly inside, or on a boundary edge, has none to test
+        if (e0 > 1e-12 && e1 > 1e-12 && e2 > 1e-12) return cur;
+        const int4 NB = __ldg(M.lnbr + cur);
+        if ((e0 > 1e-12 || NB.x < 0) && (e1 > 1e-12 || NB.y < 0) && (e2 > 1e-12 || NB.z < 0))
+            return cur;
+    }
+    const LocRes fr = flood(M.cxy, M.lnbr, M.flood_filter, cur, px, py);
+    st |= fr.st;
+    const int best = fr.tid;
+    if (best != cur) corners(M, best, P0, P1, P2);
+    return best;
+}
+
+// ---------------------------------------------------------------------------
+// K4: the walk, accel.py:138-213.  State between steps: current triangle,
+// the chosen exit edge word w and the side values (sp, sq) of its endpoints.
+// Entering neighbour N across w through N's edge j, the two shared corners
+// keep their side values (accel.py:153-159 caches them per vertex), so one
+// step loads link[N] (16 B) and the apex corner cxy[3N + j] (16 B) -- both
+// addressed by (N, j) alone.
+
+struct WalkState {
+    int cur, ei, steps;
+    uint32_t w;
+    double sp, sq;  // side values of the exit edge's endpoints, corners (ei+1)%3, (ei+2)%3
+    bool fast;      // sp < 0 < sq: the next step may take the one-candidate fast path
+};
+
+// first triangle: edges 0 (s1,s2), 1 (s2,s0), 2 (s0,s1) in order, none skipped
+__device__ __forceinline__ bool walk_first(const Ray &r, int4 L, double2 P0, double2 P1, double2 P2,
+                                           WalkState &s, uint32_t &st) {
+    double s0 = side_of(r, P0), s1 = side_of(r, P1), s2 = side_of(r, P2);
+    int best = -1, fb = -1, ncand = 0;
+    double bt = 0.0, ft = 0.0;
+#define MWT_SCAN(I, SP, SQ)                                     \
+    {                                                           \
+        double tr = (SQ) - (SP);                                \
+        if (tr > ft) { ft = tr; fb = I; }                       \
+        if ((SP) <= 0.0 && 0.0 <= (SQ)) {                       \
+            ncand++;                                            \
+            if ((SP) == 0.0 || (SQ) == 0.0) st |= ST_ZERO_SIDE; \
+            if (tr > bt) { bt = tr; best = I; }                 \
+        }                                                       \
+    }
+    MWT_SCAN(0, s1, s2)
+    MWT_SCAN(1, s2, s0)
+    MWT_SCAN(2, s0, s1)
+#undef MWT_SCAN
+    if (ncand > 1) st |= ST_MULTI;
+    if (best < 0) {
+        best = fb;
+        if (best >= 0) st |= ST_FALLBACK;
+    }
+    if (best < 0) {
+        st |= ST_ERROR;  // no exit edge: TraversalError (accel.py:190-191)
+        return false;
+    }
+    s.sp = best == 0 ? s1 : (best == 1 ? s2 : s0);
+    s.sq = best == 0 ? s2 : (best == 1 ? s0 : s1);
+    s.fast = s.sp < 0.0 && 0.0 < s.sq;
+    s.ei = best;
+    s.w = pick(L, best);
+    return true;
+}
+
+// General step rule of accel.py:171-191 for the triangle just entered through
+// its edge j: a = side of corner (j+1)%3, b = side of corner (j+2)%3 (the
+// shared corners, values carried over as the reference's per-vertex cache),
+// c = side of the apex corner j.  E1 = edge (j+1)%3 has (sp, sq) = (b, c),
+// E2 = edge (j+2)%3 has (c, a); the reference scans ascending edge index, so
+// E2 comes first iff j == 1.  Kept out of line: only degenerate or fallback
+// configurations reach it.
+// Returns the status bits | (choice + 1) << 20 with choice 0 = E1, 1 = E2, -1 = none.
+__device__ __noinline__ uint32_t walk_general(int j, double a, double b, double c, uint32_t st) {
+    const bool sw = (j == 1);
+    const double spF = sw ? c : b, sqF = sw ? a : c;
+    const double spS = sw ? b : c, sqS = sw ? c : a;
+    const double trF = sqF - spF, trS = sqS - spS;
+    const bool cF = spF <= 0.0 && 0.0 <= sqF;
+    const bool cS = spS <= 0.0 && 0.0 <= sqS;
+    int sel = -1;
+    if (cF && trF > 0.0) sel = 0;
+    if (cS && trS > (sel == 0 ? trF : 0.0)) sel = 1;
+    if (cF && cS) st |= ST_MULTI;
+    if ((cF && (spF == 0.0 || sqF == 0.0)) || (cS && (spS == 0.0 || sqS == 0.0))) st |= ST_ZERO_SIDE;
+    if (sel < 0) {  // fallback: largest positive trans (accel.py:182-184, :188-189)
+        if (trF > 0.0) sel = 0;
+        if (trS > (sel == 0 ? trF : 0.0)) sel = 1;
+        if (sel < 0) st |= ST_ERROR;
+        else st |= ST_FALLBACK;
+    }
+    const int choice = sel < 0 ? -1 : ((sel != 0) != sw ? 1 : 0);
+    return st | ((uint32_t)(choice + 1) << 20);
+}
+
+// One step into the neighbour across s.w (an internal word).  Fast path:
+// when the exit just taken was a strict candidate (sp < 0 < sq) and the new
+// apex side c is nonzero, exactly one edge qualifies -- E1 if c > 0 (its
+// trans c - sp > 0), E2 if c < 0 (trans sq - c > 0) -- with no zero side,
+// no second candidate and no fallback, which is what the general rule
+// yields in that case.
+__device__ __forceinline__ bool walk_step(const MeshDev &M, const Ray &r, WalkState &s,
+                                          uint32_t &st) {
+    if (s.steps >= 4 * M.nt + 16) {  // > #(triangle, entry) states: a revisit => TraversalError
+        st |= ST_ERROR;
+        return false;
+    }
+    s.steps++;
+    const int cur = (int)(s.w >> 2);
+    const int j = (int)(s.w & 3u);
+    const int4 L = __ldg(M.link + cur);
+    const double c = side_of(r, __ldg(M.cxy + 3 * cur + j));
+    s.cur = cur;
+    int e;
+    if (s.fast && c != 0.0) {
+        // (sp, sq) of the new exit: E1 -> (sp, c), E2 -> (c, sq)
+        if (c > 0.0) {
+            s.sq = c;
+            e = j + 1;
+        } else {
+            s.sp = c;
+            e = j + 2;
+        }
+    } else {
+        const double a = s.sq, b = s.sp;
+        const uint32_t g = walk_general(j, a, b, c, st);
+        st = g & 0xFFFFFu;
+        const int sel = (int)(g >> 20) - 1;
+        if (sel < 0) return false;
+        if (sel == 0) {  // E1
+            s.sp = b;
+            s.sq = c;
+            e = j + 1;
+        } else {  // E2
+            s.sp = c;
+            s.sq = a;
+            e = j + 2;
+        }
+        s.fast = s.sp < 0.0 && 0.0 < s.sq;
+    }
+    e = e >= 3 ? e - 3 : e;
+    s.ei = e;
+    s.w = pick(L, e);
+    return true;
+}
+
+// constrained / open exit: accel.py:192-211
+__device__ __forceinline__ int walk_terminal(const MeshDev &M, const Ray &r, const WalkState &s,
+                                          double &ot, double &ou, uint32_t &st) {
+    ot = CUDART_NAN;
+    ou = CUDART_NAN;
+    if (s.w == kOpenWord || (s.w & kBoundaryBit)) return -1;
+    const int sid = (int)(s.w & kSidMask);
+    const double4 S = ldg4d(M.seg + sid);
+    double t, u;
+    bool par = false;
+    bool ok = rsi(r, S, t, u, par);
+    if (par) st |= ST_PARALLEL;
+    if (!ok) {
+        // grazing numerical corner, accel.py:199-207
+        st |= ST_GRAZING;
+        const double2 pa = __ldg(M.cxy + 3 * s.cur + (s.ei + 1) % 3);
+        const double2 pb = __ldg(M.cxy + 3 * s.cur + (s.ei + 2) % 3);
+        const double wq = s.sp != s.sq ? s.sp / (s.sp - s.sq) : 0.5;
+        const double x = pa.x + wq * (pb.x - pa.x);
+        const double y = pa.y + wq * (pb.y - pa.y);
+        t = (x - r.ox) * r.dx + (y - r.oy) * r.dy;
+        const double ex = S.z - S.x, ey = S.w - S.y;
+        u = ((x - S.x) * ex + (y - S.y) * ey) / (ex * ex + ey * ey);  // Segment.param_of
+    }
+    const int s2 = canonical(M, r, sid, t, u, ot, ou);
+    if (s2 != sid) st |= ST_CANON;
+    return s2;
+}
+
+struct Term {
+    int seg;
+    uint32_t st;
+    double t, u;
+};
+
+// out-of-line epilogue: runs in batches at refill time
+// (everything by value: a reference to kernel-scope state would force that
+// state into local memory for the whole loop)
+__device__ __noinline__ Term terminal(const double4 *seg, const int2 *ep_range, const int32_t *ep_ids,
+                                      const double2 *cxy, double ox, double oy, double dx, double dy,
+                                      int cur, int ei, uint32_t w, double sp, double sq, uint32_t st) {
+    MeshDev M{};
+    M.seg = seg;
+    M.ep_range = ep_range;
+    M.ep_ids = ep_ids;
+    M.cxy = cxy;
+    Ray r{ox, oy, dx, dy};
+    WalkState s;
+    s.cur = cur;
+    s.ei = ei;
+    s.w = w;
+    s.sp = sp;
+    s.sq = sq;
+    Term o;
+    o.st = st;
+    o.seg = walk_terminal(M, r, s, o.t, o.u, o.st);
+    return o;
+}
+
+// ---------------------------------------------------------------------------
+// K7 histogram: block-private shared counters, flushed once per block
+
+__device__ __forceinline__ void hist_init(unsigned int *h) {
+    for (int k = threadIdx.x; k < MWT_HIST_LEN; k += blockDim.x) h[k] = 0u;
+    __syncthreads();
+}
+
+__device__ __forceinline__ void hist_add(unsigned int *h, int seg, int steps, uint32_t st) {
+    int bin = steps < MWT_HIST_STEP_BINS - 1 ? (steps < 0 ? 0 : steps) : MWT_HIST_STEP_BINS - 1;
+    atomicAdd(h + bin, 1u);
+    atomicAdd(h + (seg >= 0 ? MWT_HIST_HIT : MWT_HIST_MISS), 1u);
+    if (st) {
+        for (int b = 0; b < 11; b++)
+            if (st & (1u << b)) atomicAdd(h + MWT_HIST_STATUS0 + b, 1u);
+    }
+}
+
+__device__ __forceinline__ void hist_flush(unsigned int *h, unsigned long long steps_sum,
+                                           long long *hist) {
+    for (int o = 16; o > 0; o >>= 1) steps_sum += __shfl_down_sync(0xffffffffu, steps_sum, o);
+    if ((threadIdx.x & 31) == 0 && steps_sum)
+        atomicAdd(reinterpret_cast<unsigned long long *>(hist + MWT_HIST_STEPS_SUM), steps_sum);
+    __syncthreads();
+    for (int k = threadIdx.x; k < MWT_HIST_LEN; k += blockDim.x)
+        if (h[k] && k != MWT_HIST_STEPS_SUM)
+            atomicAdd(reinterpret_cast<unsigned long long *>(hist + k), (unsigned long long)h[k]);
+}
+
+// ---------------------------------------------------------------------------
+// the persistent trace kernel
+
+struct RaySrc {
+    int mode;          // generated rays: MWT_RAYS_*
+    Box box;
+    unsigned long long key, first;
+    const double *rays;   // loaded rays (GEN == false)
+    const int32_t *start; // optional given start triangles
+};
+
+struct TraceOut {
+    int32_t *start, *seg, *steps;
+    double *t, *u;
+    uint32_t *st;
+};
+
+// Per-ray prologue (raygen or load, locate, first triangle), out of line so
+// its temporaries do not inflate the walk loop's register budget; it runs in
+// refill batches, many lanes at once.
+struct Init {
+    double ox, oy, dx, dy, sp, sq;
+    uint32_t w, st;
+    int cur, ei, steps, phase, start;
+    bool fast;
+};
+
+template <bool GEN>
+__device__ __noinline__ Init prologue(long long i, int mode, double bx0, double by0, double bx1,
+                                      double by1, unsigned long long key, unsigned long long first,
+                                      const double *rays, const int32_t *start, int nt, int res,
+                                      int flood_filter, const double2 *cxy, const int4 *lnbr,
+                                      const int4 *link, const int32_t *anchor) {
+    MeshDev M{};
+    M.nt = nt;
+    M.res = res;
+    M.flood_filter = flood_filter;
+    M.cxy = cxy;
+    M.lnbr = lnbr;
+    M.link = link;
+    M.anchor = anchor;
+    RaySrc src{};
+    src.mode = mode;
+    src.box = Box{bx0, by0, bx1, by1};
+    src.key = key;
+    src.first = first;
+    src.rays = rays;
+    src.start = start;
+    Init o;
+    o.st = 0;
+    const Ray r = GEN ? gen_ray(src.mode, src.box, src.key, src.first + (unsigned long long)i)
+                      : load_ray(src.rays, i);
+    o.ox = r.ox; o.oy = r.oy; o.dx = r.dx; o.dy = r.dy;
+    double2 P0, P1, P2;
+    int t0;
+    if (src.start) {
+        t0 = __ldg(src.start + i);
+        if (t0 < 0 || t0 >= M.nt) t0 = -1;
+        else corners(M, t0, P0, P1, P2);
+    } else {
+        t0 = locate(M, r.ox, r.oy, o.st, P0, P1, P2);
+    }
+    o.start = t0;
+    WalkState s;
+    s.cur = t0;
+    s.steps = 1;
+    s.sp = s.sq = 0.0;
+    s.ei = 0;
+    s.w = 0;
+    s.fast = false;
+    if (t0 < 0) {
+        o.st |= ST_ERROR;
+        s.steps = 0;
+        o.phase = 3;
+    } else if (!walk_first(r, __ldg(M.link + t0), P0, P1, P2, s, o.st)) {
+        o.phase = 3;
+    } else {
+        o.phase = (s.w & kStopBit) ? 2 : 1;
+    }
+    o.sp = s.sp; o.sq = s.sq; o.w = s.w; o.cur = s.cur; o.ei = s.ei; o.steps = s.steps;
+    o.fast = s.fast;
+    return o;
+}
+
+template <bool GEN, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    k_trace(MeshDev M, RaySrc src, long long n, TraceOut out, long long *hist, int refill_below) {
+    __shared__ unsigned int h[MWT_HIST_LEN];
+    if (hist) hist_init(h);
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long chunk = (n + nwarps - 1) / nwarps;
+    long long next = warp * chunk;
+    const long long end = next + chunk < n ? next + chunk : n;
+    unsigned long long steps_sum = 0;
+
+    // lane phase: 0 idle, 1 walking, 2 reached its exit edge (terminal pending),
+    // 3 failed (TraversalError pending).  Terminals are resolved in batches at
+    // refill time so the once-per-ray epilogue also runs with many lanes.
+    int phase = 0;
+    long long idx = 0;
+    Ray r;
+    WalkState s;
+    uint32_t st = 0;
+
+    while (true) {
+        unsigned walking = __ballot_sync(FULL, phase == 1);
+        if (__popc(walking) <= refill_below) {
+            // epilogue batch: resolve every pending lane
+            if (phase >= 2) {
+                int seg = -1;
+                double t = CUDART_NAN, u = CUDART_NAN;
+                if (phase == 2) {
+                    const Term tm = terminal(M.seg, M.ep_range, M.ep_ids, M.cxy, r.ox, r.oy, r.dx,
+                                             r.dy, s.cur, s.ei, s.w, s.sp, s.sq, st);
+                    seg = tm.seg;
+                    t = tm.t;
+                    u = tm.u;
+                    st = tm.st;
+                }
+                if (out.seg) out.seg[idx] = seg;
+                if (out.t) out.t[idx] = t;
+                if (out.u) out.u[idx] = u;
+                if (out.steps) out.steps[idx] = s.steps;
+                if (out.st) out.st[idx] = st;
+                if (hist) {
+                    hist_add(h, seg, s.steps, st);
+                    steps_sum += (unsigned long long)s.steps;
+                }
+                phase = 0;
+            }
+            // prologue batch: idle lanes take the next rays of the chunk
+            if (next < end) {
+                const unsigned idle = ~walking;
+                if (phase == 0) {
+                    const long long i = next + __popc(idle & lt_mask);
+                    if (i < end) {
+                        idx = i;
+                        const Init in = prologue<GEN>(
+                            i, src.mode, src.box.x0, src.box.y0, src.box.x1, src.box.y1, src.key,
+                            src.first, src.rays, src.start, M.nt, M.res, M.flood_filter, M.cxy,
+                            M.lnbr, M.link, M.anchor);
+                        r.ox = in.ox; r.oy = in.oy; r.dx = in.dx; r.dy = in.dy;
+                        s.sp = in.sp; s.sq = in.sq; s.w = in.w;
+                        s.cur = in.cur; s.ei = in.ei; s.steps = in.steps;
+                        s.fast = in.fast;
+                        st = in.st;
+                        phase = in.phase;
+                        if (out.start) out.start[i] = in.start;
+                    }
+                }
+                next += __popc(idle);
+            }
+            walking = __ballot_sync(FULL, phase == 1);
+            if (walking == 0) {
+                if (next >= end && __ballot_sync(FULL, phase != 0) == 0) break;
+                continue;  // pending lanes resolve at the top of the loop
+            }
+        }
+        if (phase == 1) {
+            if (!walk_step(M, r, s, st)) phase = 3;
+            else if (s.w & kStopBit) phase = 2;
+        }
+    }
+    if (hist) hist_flush(h, steps_sum, hist);
+}
+
+__global__ void __launch_bounds__(kThreads) k_raygen(int mode, Box box, unsigned long long key,
+                                                     unsigned long long first, long long n,
+                                                     double *rays) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        Ray r = gen_ray(mode, box, key, first + (unsigned long long)i);
+        double2 *p = reinterpret_cast<double2 *>(rays) + 2 * i;
+        p[0] = make_double2(r.ox, r.oy);
+        p[1] = make_double2(r.dx, r.dy);
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_locate(MeshDev M, const double *pts, long long n,
+                                                     int32_t *tid, uint32_t *st) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        double2 p = __ldg(reinterpret_cast<const double2 *>(pts) + i);
+        uint32_t s = 0;
+        double2 P0, P1, P2;
+        int t = locate(M, p.x, p.y, s, P0, P1, P2);
+        if (tid) tid[i] = t;
+        if (st) st[i] = s;
+    }
+}
+
+__global__ void __launch_bounds__(kThreads) k_histogram(const int32_t *seg, const int32_t *steps,
+                                                        const uint32_t *status, long long n,
+                                                        long long *hist) {
+    __shared__ unsigned int h[MWT_HIST_LEN];
+    hist_init(h);
+    unsigned long long steps_sum = 0;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        int s = steps[i];
+        hist_add(h, seg[i], s, status ? status[i] : 0u);
+        steps_sum += (unsigned long long)(s > 0 ? s : 0);
+    }
+    hist_flush(h, steps_sum, hist);
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+
+#define MWT_LAUNCH_RET return (int)cudaGetLastError()
+
+static int g_refill_below = 16;
+static int g_min_blocks = 4;  // 4: <= 64 regs (32 warps/SM); 3: <= 80 regs (24 warps/SM)
+
+template <bool GEN, int MINB>
+static int persistent_grid(long long n) {
+    static int blocks_per_sm = 0, sms = 0;
+    if (blocks_per_sm == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_trace<GEN, MINB>, kThreads, 0);
+        if (blocks_per_sm <= 0) blocks_per_sm = 1;
+        if (sms <= 0) sms = 148;
+    }
+    long long want = (n + kThreads - 1) / kThreads;
+    long long cap = (long long)sms * blocks_per_sm;
+    return (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+}
+
+template <bool GEN, int MINB>
+static void launch_k_trace(const MeshDev &m, const RaySrc &src, long long n, const TraceOut &out,
+                           long long *hist, void *stream) {
+    k_trace<GEN, MINB><<<persistent_grid<GEN, MINB>(n), kThreads, 0, (cudaStream_t)stream>>>(
+        m, src, n, out, hist, g_refill_below);
+}
+
+template <bool GEN>
+static void launch_k_trace_any(const MeshDev &m, const RaySrc &src, long long n,
+                               const TraceOut &out, long long *hist, void *stream) {
+    if (g_min_blocks == 3)
+        launch_k_trace<GEN, 3>(m, src, n, out, hist, stream);
+    else if (g_min_blocks == 2)
+        launch_k_trace<GEN, 2>(m, src, n, out, hist, stream);
+    else
+        launch_k_trace<GEN, 4>(m, src, n, out, hist, stream);
+}
+
+int launch_raygen(int mode, const double *box, uint64_t seed, uint64_t first, int64_t n,
+                  double *rays, void *stream) {
+    if (n <= 0) return 0;
+    Box b{box[0], box[1], box[2], box[3]};
+    k_raygen<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(mode, b, ray_key(seed, mode), first,
+                                                                 n, rays);
+    MWT_LAUNCH_RET;
+}
+
+int launch_locate(const MeshDev &m, const double *pts, int64_t n, int32_t *tid, uint32_t *st,
+                  void *stream) {
+    if (n <= 0) return 0;
+    k_locate<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(m, pts, n, tid, st);
+    MWT_LAUNCH_RET;
+}
+
+int launch_trace(const MeshDev &m, const double *rays, const int32_t *start, int64_t n,
+                 int32_t *o_start, int32_t *o_seg, double *o_t, double *o_u, int32_t *o_steps,
+                 uint32_t *o_st, void *stream) {
+    if (n <= 0) return 0;
+    RaySrc src{};
+    src.rays = rays;
+    src.start = start;
+    TraceOut out{o_start, o_seg, o_steps, o_t, o_u, o_st};
+    launch_k_trace_any<false>(m, src, n, out, nullptr, stream);
+    MWT_LAUNCH_RET;
+}
+
+int launch_trace_generated(const MeshDev &m, int mode, const double *box, uint64_t seed,
+                           uint64_t first, int64_t n, int32_t *o_seg, double *o_t,
+                           int32_t *o_steps, long long *hist, void *stream) {
+    if (n <= 0) return 0;
+    RaySrc src{};
+    src.mode = mode;
+    src.box = Box{box[0], box[1], box[2], box[3]};
+    src.key = ray_key(seed, mode);
+    src.first = first;
+    TraceOut out{nullptr, o_seg, o_steps, o_t, nullptr, nullptr};
+    launch_k_trace_any<true>(m, src, n, out, hist, stream);
+    MWT_LAUNCH_RET;
+}
+
+int launch_histogram(const int32_t *seg, const int32_t *steps, const uint32_t *st, int64_t n,
+                     long long *hist, void *stream) {
+    if (n <= 0) return 0;
+    k_histogram<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(seg, steps, st, n, hist);
+    MWT_LAUNCH_RET;
+}
+
+void set_tuning(int refill_below, int min_blocks) {
+    if (refill_below >= 0) g_refill_below = refill_below > 31 ? 31 : refill_below;
+    if (min_blocks >= 2 && min_blocks <= 4) g_min_blocks = min_blocks;
+}
+
+}  // namespace mwt

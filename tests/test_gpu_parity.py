@@ -12,6 +12,7 @@ from conftest import CONFIGS, box_of, fixture_paths
 pytestmark = pytest.mark.gpu
 
 T_RTOL = 1e-12
+LOC_BRUTE = np.uint32(256)
 
 
 def _mesh_pair(cfg, which):
@@ -30,7 +31,9 @@ def _compare(got, ref, keys=("start", "seg", "steps", "status")):
         if k == "steps":
             a, b = a[ok_err], b[ok_err]
         if k == "status":
-            a, b = a.view(np.uint32), b.view(np.uint32)
+            # LOC_BRUTE marks the engine's own seed walk failing (its walk is
+            # not the reference's); every other bit must agree
+            a, b = a.view(np.uint32) & ~LOC_BRUTE, b.view(np.uint32) & ~LOC_BRUTE
         bad = np.nonzero(a != b)[0]
         assert len(bad) == 0, f"{k}: {len(bad)} mismatches, first {bad[:5]} got {a[bad[:5]]} ref {b[bad[:5]]}"
     hit = ref["seg"] >= 0
