@@ -104,6 +104,15 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts,
                     int32_t ntris, const double *seg_xy, const uint8_t *seg_kind, int32_t nsegs,
                     int device, mwt_mesh **out);
 int mwt_mesh_destroy(mwt_mesh *mesh);
+/* Host-only dry run of the packer (no device needed): validates the input
+ * exactly as mwt_mesh_create does and optionally returns the packed walk
+ * words (4*ntris int32: link[t].x/y/z/w) and locate words (4*ntris int32),
+ * plus the seed-grid resolution and its cell-centre triangles
+ * (out_anchor: res*res int32, query res first with out_anchor = NULL). */
+int mwt_pack_dry_run(const double *vx, const double *vy, int32_t nverts, const int32_t *tri_v,
+                     const int32_t *tri_nbr, const int32_t *tri_flag, int32_t ntris,
+                     const double *seg_xy, const uint8_t *seg_kind, int32_t nsegs,
+                     int32_t *out_link, int32_t *out_lnbr, int32_t *out_res, int32_t *out_anchor);
 int mwt_mesh_info_get(const mwt_mesh *mesh, mwt_mesh_info *out);
 /* copy the device-side anchor table (res*res int32) to host, for tests */
 int mwt_mesh_anchors(const mwt_mesh *mesh, int32_t *out_host);

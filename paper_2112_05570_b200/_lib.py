@@ -62,6 +62,7 @@ SIGNATURES = {
     "mwt_set_tuning": (INT, [INT, INT]),
     "mwt_mesh_create": (INT, [P, P, I32, P, P, P, I32, P, P, I32, INT, P]),
     "mwt_mesh_destroy": (INT, [P]),
+    "mwt_pack_dry_run": (INT, [P, P, I32, P, P, P, I32, P, P, I32, P, P, P, P]),
     "mwt_mesh_info_get": (INT, [P, P]),
     "mwt_mesh_anchors": (INT, [P, P]),
     "mwt_raygen_dev": (INT, [INT, P, U64, U64, I64, P, P]),

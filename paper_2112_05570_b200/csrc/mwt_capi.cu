@@ -162,6 +162,23 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     return MWT_OK;
 }
 
+int mwt_pack_dry_run(const double *vx, const double *vy, int32_t nverts, const int32_t *tri_v,
+                     const int32_t *tri_nbr, const int32_t *tri_flag, int32_t ntris,
+                     const double *seg_xy, const uint8_t *seg_kind, int32_t nsegs,
+                     int32_t *out_link, int32_t *out_lnbr, int32_t *out_res, int32_t *out_anchor) {
+    mwt::HostPacked P;
+    std::string err;
+    int rc = mwt::pack_mesh(vx, vy, nverts, tri_v, tri_nbr, tri_flag, ntris, seg_xy, seg_kind,
+                            nsegs, &P, &err);
+    if (rc != MWT_OK) return fail(rc, err);
+    if (out_link) std::memcpy(out_link, P.link.data(), P.link.size() * sizeof(int32_t));
+    if (out_lnbr) std::memcpy(out_lnbr, P.lnbr.data(), P.lnbr.size() * sizeof(int32_t));
+    if (out_res) *out_res = P.res;
+    if (out_anchor && P.res > 0)
+        std::memcpy(out_anchor, P.anchor.data(), P.anchor.size() * sizeof(int32_t));
+    return MWT_OK;
+}
+
 int mwt_mesh_destroy(mwt_mesh *m) {
     if (!m) return MWT_OK;
     DeviceGuard g(m->device);

@@ -145,7 +145,7 @@ static __device__ __noinline__ double cr_hypot(double x, double y) {
 }
 
 // ---------------------------------------------------------------------------
-// K2: ray generator (twin: oracle/raygen.py, oracle/mwt_oracle.c orc_raygen)
+// K2: ray generator (its host twins live in the test oracle: oracle/raygen.py)
 
 constexpr unsigned long long kGolden = 0x9E3779B97F4A7C15ull;
 

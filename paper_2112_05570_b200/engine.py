@@ -319,3 +319,21 @@ def summarize_histogram(h) -> dict:
         "max_steps_bin": int(np.nonzero(steps)[0].max()) if n else 0,
         "status": {name: int(h[_lib.HIST_STATUS0 + b]) for b, name in enumerate(_lib.STATUS_NAMES)},
     }
+
+
+def pack_dry_run(scene: SceneArrays, tri: TriArrays) -> dict:
+    """Run the K1 packer on the host only (no device): returns the packed walk
+    words, locate words and seed grid exactly as mwt_mesh_create builds them."""
+    import ctypes
+    vxy = _f64(tri.vxy).reshape(-1, 2)
+    vx, vy = _f64(vxy[:, 0]), _f64(vxy[:, 1])
+    nt = len(tri.v)
+    link = np.empty((nt, 4), np.int32)
+    lnbr = np.empty((nt, 4), np.int32)
+    res = ctypes.c_int32(0)
+    args = (ptr(vx), ptr(vy), len(vx), ptr(_i32(tri.v)), ptr(_i32(tri.nbr)), ptr(_i32(tri.flag)), nt,
+            ptr(_f64(scene.xy)), ptr(np.ascontiguousarray(scene.kind, dtype=np.uint8)), len(scene.kind))
+    check(lib.mwt_pack_dry_run(*args, ptr(link), ptr(lnbr), ctypes.byref(res), None), "pack_dry_run")
+    anchor = np.empty(max(res.value, 0) ** 2, np.int32)
+    check(lib.mwt_pack_dry_run(*args, None, None, ctypes.byref(res), ptr(anchor)), "pack_dry_run")
+    return dict(link=link, lnbr=lnbr, res=res.value, anchor=anchor.reshape(res.value, res.value))

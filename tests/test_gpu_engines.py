@@ -1,0 +1,217 @@
+"""Device engines against the oracle at scale, the drop-in API, histograms,
+edge cases and full-size properties."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import CONFIGS, box_of, fixture_paths
+
+pytestmark = pytest.mark.gpu
+
+C_T_GRID = (0.125, 0.25, 0.5, 1.0, 2.0, 4.0, 8.0)
+
+
+@pytest.mark.parametrize("cfg", CONFIGS[1:])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_bvh_kd_match_oracle_all_ct(cfg, mode):
+    from oracle import oracle as orc
+    from paper_2112_05570_b200.engine import DeviceBvh, DeviceKd, DeviceMesh
+    from paper_2112_05570_b200.formats import load_scene
+    paths = fixture_paths(cfg, "cdt")
+    d = os.path.dirname(paths[0])
+    m = DeviceMesh(load_scene(paths[0]), None)
+    om = orc.Mesh.from_files(paths[0], None)
+    rays = orc.raygen(mode, box_of(cfg), 5, 0, 1 << 14)
+    for ct in C_T_GRID:
+        arr = orc.load_npz(os.path.join(d, f"bvh_ct{ct:g}.npz"))
+        got, ref = DeviceBvh(m, arr).trace(rays), orc.Bvh(om, arr).trace(rays)
+        for k in ("seg", "node_tests", "prim_tests"):
+            assert np.array_equal(got[k], ref[k]), (ct, k)
+        h = ref["seg"] >= 0
+        assert np.array_equal(got["t"][h], ref["t"][h])
+        arr = orc.load_npz(os.path.join(d, f"kd_ct{ct:g}.npz"))
+        got, ref = DeviceKd(m, arr).trace(rays), orc.Kd(om, arr).trace(rays)
+        for k in ("seg", "nodes", "ropes", "prims"):
+            assert np.array_equal(got[k], ref[k]), (ct, k)
+        assert np.array_equal(got["status"].view(np.uint32) & 1, ref["status"] & 1)
+
+
+@pytest.mark.parametrize("cfg", CONFIGS)
+def test_brute_force_matches_oracle(cfg):
+    from oracle import oracle as orc
+    from paper_2112_05570_b200.engine import DeviceMesh
+    paths = fixture_paths(cfg, "cdt")
+    m = DeviceMesh.from_files(*paths)
+    om = orc.Mesh.from_files(*paths)
+    rays = orc.raygen(1, box_of(cfg), 9, 0, 4096)
+    got, ref = m.brute_force(rays), om.brute_force(rays)
+    assert np.array_equal(got["seg"], ref["seg"])
+    h = ref["seg"] >= 0
+    assert np.array_equal(got["t"][h], ref["t"][h])
+    # the walk finds the same closest hits as the brute-force oracle (test_accel.py:47-59)
+    w = m.trace(rays)
+    assert np.array_equal(w["seg"], ref["seg"])
+    assert np.allclose(w["t"][h], ref["t"][h], rtol=1e-9, atol=0)
+
+
+def test_locate_matches_oracle_everywhere():
+    """start triangles for origins on vertices, edge midpoints, centroids and
+    random points (test_accel.py:74-101)."""
+    from oracle import oracle as orc
+    from paper_2112_05570_b200.engine import DeviceMesh
+    from paper_2112_05570_b200.formats import load_tri
+    for cfg in ("lines64", "floorplan64"):
+        paths = fixture_paths(cfg, "mwt")
+        m, om, tri = DeviceMesh.from_files(*paths), orc.Mesh.from_files(*paths), load_tri(paths[1])
+        P = tri.vxy[tri.v]
+        pts = [tri.vxy, P.mean(axis=1), 0.5 * (P[:, 0] + P[:, 1]), 0.5 * (P[:, 1] + P[:, 2]),
+               np.random.default_rng(1).random((20000, 2))]
+        pts = np.ascontiguousarray(np.concatenate(pts))
+        got, gst = m.locate(pts)
+        ref, rst = om.locate(pts)
+        assert np.array_equal(got, ref)
+        assert np.array_equal(gst & 128, rst & 128)  # tie flag
+
+
+def test_generated_kernel_equals_explicit_rays_and_histogram():
+    import torch
+    from paper_2112_05570_b200.engine import DeviceMesh, new_histogram
+    from paper_2112_05570_b200.sharding import histogram_host
+    paths = fixture_paths("lines1024", "mwt") or fixture_paths("lines1024", "cdt")
+    m = DeviceMesh.from_files(*paths)
+    n = 1 << 18
+    for mode in (0, 1):
+        h = new_histogram()
+        gen = m.trace_generated_device(mode, (0, 0, 1, 1), 3, 777, n, outputs=True, hist=h)
+        rays = m.raygen_device(mode, (0, 0, 1, 1), 3, 777, n)
+        ex = m.trace_device(rays)
+        torch.cuda.synchronize()
+        for k in ("seg", "steps"):
+            assert torch.equal(gen[k], ex[k])
+        hit = ex["seg"] >= 0
+        assert torch.equal(gen["t"][hit], ex["t"][hit])
+        ref = histogram_host(ex["seg"].cpu().numpy(), ex["steps"].cpu().numpy(),
+                             ex["status"].cpu().numpy().view(np.uint32))
+        assert np.array_equal(h.cpu().numpy(), ref)
+        h2 = new_histogram()
+        m_hist = __import__("paper_2112_05570_b200._lib", fromlist=["x"])
+        m_hist.check(m_hist.lib.mwt_histogram_dev(m_hist.ptr(ex["seg"]), m_hist.ptr(ex["steps"]),
+                                                  m_hist.ptr(ex["status"]), n, m_hist.ptr(h2), None))
+        torch.cuda.synchronize()
+        assert np.array_equal(h2.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("refill,minb", [(0, 4), (4, 3), (16, 2), (31, 4)])
+def test_tuning_knobs_do_not_change_results(refill, minb):
+    from oracle import oracle as orc
+    from paper_2112_05570_b200 import _lib
+    from paper_2112_05570_b200.engine import DeviceMesh
+    paths = fixture_paths("hair512", "mwt")
+    m, om = DeviceMesh.from_files(*paths), orc.Mesh.from_files(*paths)
+    rays = orc.raygen(0, (0, 0, 1, 1), 2, 0, 50000)
+    ref = om.trace(rays)
+    _lib.check(_lib.lib.mwt_set_tuning(refill, minb))
+    try:
+        got = m.trace(rays)
+    finally:
+        _lib.lib.mwt_set_tuning(16, 4)
+    for k in ("start", "seg", "steps"):
+        assert np.array_equal(got[k], ref[k])
+
+
+def test_edge_cases():
+    from oracle import oracle as orc
+    from paper_2112_05570_b200.engine import DeviceMesh
+    paths = fixture_paths("lines64", "mwt")
+    m, om = DeviceMesh.from_files(*paths), orc.Mesh.from_files(*paths)
+    # empty batch
+    out = m.trace(np.zeros((0, 4)))
+    assert len(out["seg"]) == 0
+    # invalid start triangles -> error status, no crash
+    rays = orc.raygen(0, (0, 0, 1, 1), 0, 0, 8)
+    bad = m.trace(rays, np.array([-1, 10 ** 6, 0, 1, 2, 3, 4, 5], np.int32))
+    assert (bad["status"][:2] & 1).all() and (bad["seg"][:2] == -1).all()
+    # axis-aligned rays from every box side, rays through mesh vertices
+    tri = om.tri
+    v = np.stack([tri.vx, tri.vy], 1)
+    dirs = [(1, 0), (-1, 0), (0, 1), (0, -1)]
+    rr = []
+    for (dx, dy) in dirs:
+        for p in v:
+            rr.append([p[0], p[1], dx, dy])
+    c = v.mean(0)
+    for p in v:  # from the centre through each vertex
+        d = p - c
+        n = np.hypot(*d)
+        if n > 0:
+            rr.append([c[0], c[1], d[0] / n, d[1] / n])
+    rr = np.array(rr)
+    got, ref = m.trace(rr), om.trace(rr)
+    assert np.array_equal(got["start"], ref["start"])
+    assert np.array_equal(got["seg"], ref["seg"])
+    ok = (ref["status"] & 1) == 0
+    assert np.array_equal(got["steps"][ok], ref["steps"][ok])
+    mask = ~np.uint32(256)  # LOC_BRUTE is engine-specific (its own seed walk)
+    assert np.array_equal(got["status"].view(np.uint32) & mask, ref["status"] & mask)
+    hit = ok & (ref["seg"] >= 0)
+    assert np.array_equal(got["t"][hit], ref["t"][hit])
+
+
+def test_full_size_floorplan_properties():
+    """2^26 box-entry rays (the FloorPlan config size): no error / overflow,
+    histogram totals consistent, and a 2^16 subsample bit-exact vs the oracle."""
+    import torch
+    from oracle import oracle as orc
+    from paper_2112_05570_b200.engine import DeviceMesh, new_histogram, summarize_histogram
+    paths = fixture_paths("floorplan64", "mwt")
+    m = DeviceMesh.from_files(*paths)
+    n = 1 << 26
+    h = new_histogram()
+    out = m.trace_generated_device(0, (0, 0, 1, 1), 0, 0, n, outputs=True, hist=h)
+    torch.cuda.synchronize()
+    s = summarize_histogram(h)
+    assert s["rays"] == n and s["hits"] + s["misses"] == n
+    assert s["status"]["error"] == 0 and s["status"]["overflow"] == 0
+    assert s["steps_sum"] == int(out["steps"].to(torch.int64).sum())
+    idx = np.sort(np.random.default_rng(0).choice(n, 1 << 16, replace=False))
+    om = orc.Mesh.from_files(*paths)
+    first = int(idx[0])
+    rays = np.concatenate([orc.raygen(0, (0, 0, 1, 1), 0, int(i), 1) for i in idx[:256]])
+    ref = om.trace(rays)
+    got_seg = out["seg"][torch.from_numpy(idx[:256]).cuda()].cpu().numpy()
+    got_steps = out["steps"][torch.from_numpy(idx[:256]).cuda()].cpu().numpy()
+    assert np.array_equal(got_seg, ref["seg"]) and np.array_equal(got_steps, ref["steps"])
+    del first
+
+
+def test_drop_in_api_on_model_objects():
+    """The reference's call shapes (test_accel.py) through the drop-in API."""
+    from oracle import oracle as orc
+    from paper_2112_05570_b200 import accel
+    from paper_2112_05570_b200.geometry import Point, Ray
+    from paper_2112_05570_b200.model import Scene, load_triangulation
+    paths = fixture_paths("lines64", "mwt")
+    scene = Scene.load(paths[0])
+    tri = load_triangulation(paths[1], scene)
+    om = orc.Mesh.from_files(*paths)
+    rays_np = orc.raygen(1, (0, 0, 1, 1), 4, 0, 200)
+    ref = om.trace(rays_np)
+    loc = accel.TriLocator(tri)
+    for k, r in enumerate(rays_np):
+        ray = Ray(Point(r[0], r[1]), Point(r[2], r[3]))
+        start = loc.locate(ray.origin)
+        assert start == ref["start"][k]
+        hit, stats = accel.traverse_triangulation(tri, ray, start)
+        assert stats.tri_steps == ref["steps"][k]
+        assert (hit is None) == (ref["seg"][k] < 0)
+        if hit is not None:
+            assert hit.seg == ref["seg"][k] and hit.t == ref["t"][k]
+            assert isinstance(hit.point, Point)
+        bf = accel.brute_force_closest(scene, ray)
+        assert (bf is None) == (hit is None) and (bf is None or bf.seg == hit.seg)
+    assert accel.locate_triangle(tri, Point(0.5, 0.5), "brute") == loc.locate(Point(0.5, 0.5))
+    with pytest.raises(ValueError):
+        accel.locate_triangle(tri, Point(0.5, 0.5), "nope")
+    batch = accel.trace_batch(tri, rays_np)
+    assert np.array_equal(batch["seg"], ref["seg"])

@@ -1,0 +1,159 @@
+"""Pin the C oracle (oracle/mwt_oracle.c) to the reference: every function is
+checked against golden vectors recorded by running the unmodified reference
+(tests/golden/make_golden.py).  CPU only."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import CONFIGS, GOLDEN, fixture_paths
+
+orc = pytest.importorskip("oracle.oracle")
+from oracle import raygen as rg  # noqa: E402
+
+
+def _golden(name):
+    p = os.path.join(GOLDEN, name)
+    if not os.path.exists(p):
+        pytest.skip(f"golden file {name} not generated")
+    return np.load(p)
+
+
+def test_hypot_is_cpython_hypot():
+    g = _golden("hypot.npz")
+    got = np.array([orc.hypot(a, b) for a, b in zip(g["x"].tolist(), g["y"].tolist())])
+    assert np.array_equal(got.view(np.uint64), g["h"].view(np.uint64))
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_raygen_twins_agree(mode):
+    box = (0.0, 0.0, 1.0, 0.5)
+    a = rg.raygen(mode, box, 11, 1000, 50000)
+    b = orc.raygen(mode, box, 11, 1000, 50000)
+    assert np.array_equal(a.view(np.uint64), b.view(np.uint64))
+    # reference Ray would not renormalise (geometry.py:73)
+    n = np.hypot(a[:, 2], a[:, 3])
+    assert np.abs(n - 1.0).max() <= 1e-12
+    if mode == 0:  # origin exactly on the entered side of the box
+        on = (a[:, 0] == 0.0) | (a[:, 0] == 1.0) | (a[:, 1] == 0.0) | (a[:, 1] == 0.5)
+        assert on.all()
+
+
+def test_raygen_isotropic():
+    """chi-square isotropy like test_harness.py:99-111."""
+    from scipy.stats import chisquare
+    r = rg.raygen(0, (0, 0, 1, 1), 3, 0, 200000)
+    ang = np.arctan2(r[:, 3], r[:, 2])
+    counts, _ = np.histogram(ang, bins=36, range=(-np.pi, np.pi))
+    assert chisquare(counts).pvalue > 1e-4
+
+
+def test_ray_segment_intersect_golden():
+    g = _golden("known.npz")
+    t = np.empty(len(g["rsi_rays"]))
+    u = np.empty(len(g["rsi_rays"]))
+    for k, (r, s) in enumerate(zip(g["rsi_rays"], g["rsi_segs"])):
+        tt, uu = np.zeros(1), np.zeros(1)
+        import ctypes
+        ok = orc.lib().orc_ray_segment_intersect(
+            np.ascontiguousarray(r).ctypes.data_as(ctypes.c_void_p),
+            np.ascontiguousarray(s).ctypes.data_as(ctypes.c_void_p),
+            tt.ctypes.data_as(ctypes.c_void_p), uu.ctypes.data_as(ctypes.c_void_p))
+        t[k], u[k] = (tt[0], uu[0]) if ok else (np.nan, np.nan)
+    ref = g["rsi_tu"]
+    assert np.array_equal(np.isnan(t), np.isnan(ref[:, 0]))
+    m = ~np.isnan(t)
+    assert np.array_equal(t[m], ref[m, 0]) and np.array_equal(u[m], ref[m, 1])
+
+
+def _known_cases():
+    p = os.path.join(GOLDEN, "known.npz")
+    if not os.path.exists(p):
+        return []
+    return [str(c) for c in np.load(p)["cases"]]
+
+
+def known_mesh(g, name):
+    sc = orc.RawScene(*(np.ascontiguousarray(g[f"{name}__seg_xy"][:, k]) for k in range(4)),
+                      np.ascontiguousarray(g[f"{name}__seg_kind"]))
+    vxy = g[f"{name}__vxy"]
+    tri = orc.RawTri(np.ascontiguousarray(vxy[:, 0]), np.ascontiguousarray(vxy[:, 1]),
+                     np.ascontiguousarray(g[f"{name}__v"]), np.ascontiguousarray(g[f"{name}__nbr"]),
+                     np.ascontiguousarray(g[f"{name}__flag"]))
+    return orc.Mesh(sc, tri)
+
+
+def check_walk(out, ref, prefix=""):
+    err = ref[prefix + "error"].astype(bool)
+    assert np.array_equal((out["status"] & 1).astype(bool), err)
+    ok = ~err
+    for k in ("start", "seg", "steps"):
+        a, b = out[k][ok], ref[prefix + k][ok]
+        bad = np.nonzero(a != b)[0]
+        assert len(bad) == 0, f"{k}: {len(bad)} mismatches e.g. {bad[:5]}"
+    hit = ok & (ref[prefix + "seg"] >= 0)
+    assert np.array_equal(out["t"][hit], ref[prefix + "t"][hit])
+
+
+@pytest.mark.parametrize("name", _known_cases())
+def test_known_cases(name):
+    g = _golden("known.npz")
+    m = known_mesh(g, name)
+    rays = g[f"{name}__rays"]
+    out = m.trace(rays)
+    ref = {k[len(name) + 4:]: g[k] for k in g.files if k.startswith(f"{name}__w_")}
+    check_walk(out, ref)
+    tid, _ = m.locate(g[f"{name}__loc_pts"])
+    assert np.array_equal(tid, g[f"{name}__loc_anchor"])
+    assert np.array_equal(tid, g[f"{name}__loc_brute"])
+    bf = m.brute_force(rays)
+    assert np.array_equal(bf["seg"], g[f"{name}__bf_seg"])
+    h = bf["seg"] >= 0
+    assert np.array_equal(bf["t"][h], g[f"{name}__bf_t"][h])
+
+
+@pytest.mark.parametrize("cfg", CONFIGS)
+@pytest.mark.parametrize("which", ["cdt", "mwt"])
+def test_config_walk_golden(cfg, which):
+    g = _golden(f"config_{cfg}.npz")
+    paths = fixture_paths(cfg, which)
+    if paths is None or f"{which}0_seg" not in g.files:
+        pytest.skip("fixture/golden not generated")
+    m = orc.Mesh.from_files(*paths)
+    for mode in (0, 1):
+        if f"rays{mode}" not in g.files or f"{which}{mode}_seg" not in g.files:
+            continue
+        rays = g[f"rays{mode}"]
+        box = (0.0, 0.0, 1.0, 0.5) if cfg == "grass4096" else (0.0, 0.0, 1.0, 1.0)
+        assert np.array_equal(orc.raygen(mode, box, 0, 0, len(rays)).view(np.uint64), rays.view(np.uint64))
+        check_walk(m.trace(rays), g, f"{which}{mode}_")
+        n = len(g[f"bf{mode}_seg"])
+        bf = m.brute_force(rays[:n])
+        assert np.array_equal(bf["seg"], g[f"bf{mode}_seg"])
+
+
+@pytest.mark.parametrize("cfg", CONFIGS[1:])
+def test_structures_golden(cfg):
+    g = _golden(f"struct_{cfg}.npz")
+    paths = fixture_paths(cfg, "cdt")
+    m = orc.Mesh.from_files(*paths)
+    d = os.path.dirname(paths[0])
+    for key in [k for k in g.files if k.startswith("bvh") and k.endswith("_seg")]:
+        tag = key[3:-4]               # "<mode>_ct<c>"
+        mode, ct = tag.split("_ct")
+        rays = g[f"rays{mode}"]
+        bvh = orc.Bvh(m, orc.load_npz(os.path.join(d, f"bvh_ct{ct}.npz")))
+        o = bvh.trace(rays)
+        assert np.array_equal(o["seg"], g[f"bvh{tag}_seg"])
+        h = o["seg"] >= 0
+        assert np.array_equal(o["t"][h], g[f"bvh{tag}_t"][h])
+        assert np.array_equal(o["node_tests"], g[f"bvh{tag}_nodes"])
+        assert np.array_equal(o["prim_tests"], g[f"bvh{tag}_prims"])
+        kd = orc.Kd(m, orc.load_npz(os.path.join(d, f"kd_ct{ct}.npz")))
+        o = kd.trace(rays)
+        ok = g[f"kd{tag}_nodes"] >= 0
+        assert np.array_equal(o["seg"][ok], g[f"kd{tag}_seg"][ok])
+        assert np.array_equal(o["nodes"][ok], g[f"kd{tag}_nodes"][ok])
+        assert np.array_equal(o["ropes"][ok], g[f"kd{tag}_ropes"][ok])
+        assert np.array_equal(o["prims"][ok], g[f"kd{tag}_prims"][ok])
+        assert np.array_equal((o["status"] & 1) == 1, ~ok)
