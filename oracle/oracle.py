@@ -256,7 +256,7 @@ class Kd:
         self.mesh = mesh
         a = {k: np.ascontiguousarray(v) for k, v in arrays.items()}
         self._a = a
-        self.h = lib().orc_kd_create(len(a["axis"]), int(a["num_leaves"]), _p(a["axis"]), _p(a["pos"]),
+        self.h = lib().orc_kd_create(len(a["axis"]), int(np.asarray(a["num_leaves"]).reshape(-1)[0]), _p(a["axis"]), _p(a["pos"]),
                                      _p(a["left"]), _p(a["right"]), _p(a["box"]), _p(a["ropes"]),
                                      _p(a["rope_cost"]), _p(a["prim_off"]), _p(a["prim_cnt"]),
                                      _p(a["prims"]))

@@ -103,7 +103,24 @@ class _TriMap:
         self.arrays = TriArrays(vxy, v, nbr, flag)
 
 
-_mesh_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+class _IdCache:
+    """Per-object cache keyed by identity (the reference's Scene and
+    Triangulation are unhashable dataclasses); entries die with the object."""
+
+    def __init__(self):
+        self._d: dict = {}
+
+    def get(self, obj):
+        got = self._d.get(id(obj))
+        return got[1] if got is not None and got[0]() is obj else None
+
+    def __setitem__(self, obj, value):
+        key = id(obj)
+        self._d[key] = (weakref.ref(obj), value)
+        weakref.finalize(obj, self._d.pop, key, None)
+
+
+_mesh_cache = _IdCache()
 
 
 class _Packed:
@@ -292,8 +309,8 @@ def flatten_kd(kd) -> dict:
                 prims=np.array(prims, np.int32))
 
 
-_struct_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
-_scene_mesh_cache: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+_struct_cache = _IdCache()
+_scene_mesh_cache = _IdCache()
 
 
 def _scene_mesh(scene) -> DeviceMesh:

@@ -36,7 +36,7 @@ namespace mwt {
 #define ST_OVERFLOW MWT_ST_OVERFLOW
 
 constexpr int kThreads = 256;
-constexpr int kFloodCap = 32;
+constexpr int kFloodCap = 160;  // > the largest vertex fan of every fixture (64, FloorPlan corner)
 constexpr int kBvhStack = 128;
 constexpr int kKdMailbox = 512;
 
