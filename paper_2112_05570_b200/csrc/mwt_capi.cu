@@ -115,6 +115,7 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     if (!g.ok) return fail(MWT_E_CUDA, "mesh_create: cannot select device " + std::to_string(device));
     const size_t nt = P.nt > 0 ? P.nt : 1, ns = P.ns > 0 ? P.ns : 1;
     size_t bytes = Arena::align(nt * 16) + Arena::align(nt * 48) + Arena::align(nt * 16) +
+                   Arena::align(nt * 96) +
                    Arena::align(ns * 32) + Arena::align(ns) + Arena::align(ns * 2 * 8) +
                    Arena::align(P.ep_ids.size() * 4) + Arena::align(P.anchor.size() * 4);
     Arena a;
@@ -125,6 +126,7 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     m->blob = a.base;
     int4 *link = carve<int4>(a, nt);
     double2 *cxy = carve<double2>(a, 3 * nt);
+    int4 *step = carve<int4>(a, 6 * nt);
     int4 *lnbr = carve<int4>(a, nt);
     double4 *seg = carve<double4>(a, ns);
     uint8_t *kind = carve<uint8_t>(a, ns);
@@ -137,6 +139,7 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     };
     up(link, P.link.data(), (size_t)P.nt * 16);
     up(cxy, P.cxy.data(), (size_t)P.nt * 48);
+    up(step, P.step.data(), (size_t)P.nt * 96);
     up(lnbr, P.lnbr.data(), (size_t)P.nt * 16);
     up(seg, P.seg.data(), (size_t)P.ns * 32);
     up(kind, P.segkind.data(), (size_t)P.ns);
@@ -149,7 +152,7 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
         delete m;
         return cuda_fail(e, "mesh_create: upload");
     }
-    m->dev = mwt::MeshDev{P.nt, P.ns, P.res, P.flood_filter, link, cxy, lnbr, seg, kind, epr, epi, anc};
+    m->dev = mwt::MeshDev{P.nt, P.ns, P.res, P.flood_filter, link, cxy, step, lnbr, seg, kind, epr, epi, anc};
     m->info.num_vertices = P.nv;
     m->info.num_triangles = P.nt;
     m->info.num_segments = P.ns;

@@ -36,7 +36,11 @@ namespace mwt {
 //   anchor[res*res] int32 seed grid over [0,1]^2: triangle holding each cell
 //                   centre (Triangulation.locate, trimesh.py:386-416), row-major.
 //
-// One walk step reads link[N] (16 B) + cxy[3N+j] (16 B) = 32 algorithmic B.
+//   step[3T] 32-B step records, one per (triangle N, entry edge j) at 3N+j:
+//                   {word of edge (j+1)%3, word of edge (j+2)%3, 0, 0 | apex
+//                   corner j (x, y)} -- everything one walk step needs, in one
+//                   32-B sector.  A step reads exactly one record: 32
+//                   algorithmic bytes per triangle entered.
 // ---------------------------------------------------------------------------
 
 constexpr uint32_t kStopBit = 0x80000000u;
@@ -49,6 +53,7 @@ struct HostPacked {
     int32_t res = 0, anchors_not_strict = 0, flood_filter = 1;
     std::vector<int32_t> link;      // 4*nt
     std::vector<double> cxy;        // 6*nt
+    std::vector<int32_t> step;      // 8*3*nt (32-B records)
     std::vector<int32_t> lnbr;      // 4*nt
     std::vector<double> seg;        // 4*ns
     std::vector<uint8_t> segkind;   // ns
@@ -68,6 +73,7 @@ struct MeshDev {
     int32_t nt, ns, res, flood_filter;
     const int4 *link;
     const double2 *cxy;
+    const int4 *step;  // record k occupies step[2k] (words) and step[2k+1] (apex as double2)
     const int4 *lnbr;
     const double4 *seg;
     const uint8_t *segkind;

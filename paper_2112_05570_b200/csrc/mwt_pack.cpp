@@ -134,6 +134,15 @@ int pack_mesh(const double *vx, const double *vy, int32_t nv, const int32_t *tv,
             P.link[4LL * t + i] = (int32_t)w;
         }
     }
+    // per-(triangle, entry edge) step records
+    P.step.assign(8LL * 3 * nt, 0);
+    for (int t = 0; t < nt; t++)
+        for (int j = 0; j < 3; j++) {
+            int32_t *r = P.step.data() + 8LL * (3LL * t + j);
+            r[0] = P.link[4LL * t + (j + 1) % 3];
+            r[1] = P.link[4LL * t + (j + 2) % 3];
+            std::memcpy(r + 4, &P.cxy[6LL * t + 2 * j], 16);
+        }
     P.seg.assign(seg_xy, seg_xy + 4LL * ns);
     P.segkind.assign(seg_kind, seg_kind + ns);
 

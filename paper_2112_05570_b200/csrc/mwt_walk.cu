@@ -203,6 +203,13 @@ struct WalkState {
     bool fast;      // sp < 0 < sq: the next step may take the one-candidate fast path
 };
 
+// the 32-B step record for entering triangle w >> 2 through its edge w & 3
+__device__ __forceinline__ void load_step(const MeshDev &M, uint32_t w, int4 &W, double2 &A) {
+    const int k = 3 * (int)(w >> 2) + (int)(w & 3u);
+    W = __ldg(M.step + 2 * k);
+    A = __ldg(reinterpret_cast<const double2 *>(M.step + 2 * k + 1));
+}
+
 // first triangle: edges 0 (s1,s2), 1 (s2,s0), 2 (s0,s1) in order, none skipped
 __device__ __forceinline__ bool walk_first(const Ray &r, int4 L, double2 P0, double2 P1, double2 P2,
                                            WalkState &s, uint32_t &st) {
@@ -239,6 +246,7 @@ __device__ __forceinline__ bool walk_first(const Ray &r, int4 L, double2 P0, dou
     s.w = pick(L, best);
     return true;
 }
+
 
 // General step rule of accel.py:171-191 for the triangle just entered through
 // its edge j: a = side of corner (j+1)%3, b = side of corner (j+2)%3 (the
@@ -285,8 +293,12 @@ __device__ __forceinline__ bool walk_step(const MeshDev &M, const Ray &r, WalkSt
     s.steps++;
     const int cur = (int)(s.w >> 2);
     const int j = (int)(s.w & 3u);
-    const int4 L = __ldg(M.link + cur);
-    const double c = side_of(r, __ldg(M.cxy + 3 * cur + j));
+    // one 32-B step record: both candidate exit words and the apex corner
+    int4 W;
+    double2 A;
+    load_step(M, s.w, W, A);
+    const uint32_t w1 = (uint32_t)W.x, w2 = (uint32_t)W.y;  // edges (j+1)%3, (j+2)%3
+    const double c = side_of(r, A);
     s.cur = cur;
     int e;
     if (s.fast && c != 0.0) {
@@ -294,10 +306,14 @@ __device__ __forceinline__ bool walk_step(const MeshDev &M, const Ray &r, WalkSt
         if (c > 0.0) {
             s.sq = c;
             e = j + 1;
+            s.w = w1;
         } else {
             s.sp = c;
             e = j + 2;
+            s.w = w2;
         }
+        s.ei = e >= 3 ? e - 3 : e;
+        return true;
     } else {
         const double a = s.sq, b = s.sp;
         const uint32_t g = walk_general(j, a, b, c, st);
@@ -308,16 +324,16 @@ __device__ __forceinline__ bool walk_step(const MeshDev &M, const Ray &r, WalkSt
             s.sp = b;
             s.sq = c;
             e = j + 1;
+            s.w = w1;
         } else {  // E2
             s.sp = c;
             s.sq = a;
             e = j + 2;
+            s.w = w2;
         }
         s.fast = s.sp < 0.0 && 0.0 < s.sq;
     }
-    e = e >= 3 ? e - 3 : e;
-    s.ei = e;
-    s.w = pick(L, e);
+    s.ei = e >= 3 ? e - 3 : e;
     return true;
 }
 
