@@ -84,11 +84,13 @@ typedef struct {
 int mwt_abi_version(void);
 const char *mwt_last_error(void);
 int mwt_device_count(int *count);
-/* Tuning knobs of the persistent walk kernel (process-wide; -1 = keep):
- * idle lanes of a warp refill once at most `refill_below` lanes are still
- * walking (default 16); `min_blocks_per_sm` in {2,3,4} selects the register
- * budget of the compiled variant (256-thread CTAs; default 4 = 64 regs). */
-int mwt_set_tuning(int refill_below, int min_blocks_per_sm);
+/* Tuning knobs of the persistent walk kernel (process-wide; -1 = keep).
+ * `variant` 1 = refill batches (default): idle lanes refill once at most
+ * `refill_below` (default 4) lanes still walk; 0 = per-warp shared-memory
+ * queues with bulk prologue/epilogue.  `min_blocks_per_sm` in {2,3,4}
+ * selects the register budget of the compiled kernel (256-thread CTAs;
+ * default 3 = 80 registers). */
+int mwt_set_tuning(int refill_below, int min_blocks_per_sm, int variant);
 
 /* K1 -- mesh packer.
  * Replaces: building `Triangulation` + `SceneIndex` for the walk

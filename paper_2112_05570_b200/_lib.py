@@ -59,7 +59,7 @@ SIGNATURES = {
     "mwt_abi_version": (INT, []),
     "mwt_last_error": (ctypes.c_char_p, []),
     "mwt_device_count": (INT, [P]),
-    "mwt_set_tuning": (INT, [INT, INT]),
+    "mwt_set_tuning": (INT, [INT, INT, INT]),
     "mwt_mesh_create": (INT, [P, P, I32, P, P, P, I32, P, P, I32, INT, P]),
     "mwt_mesh_destroy": (INT, [P]),
     "mwt_pack_dry_run": (INT, [P, P, I32, P, P, P, I32, P, P, I32, P, P, P, P]),

@@ -87,8 +87,8 @@ extern "C" {
 
 int mwt_abi_version(void) { return MWT_ABI_VERSION; }
 
-int mwt_set_tuning(int refill_below, int min_blocks_per_sm) {
-    mwt::set_tuning(refill_below, min_blocks_per_sm);
+int mwt_set_tuning(int refill_below, int min_blocks_per_sm, int variant) {
+    mwt::set_tuning(refill_below, min_blocks_per_sm, variant);
     return MWT_OK;
 }
 

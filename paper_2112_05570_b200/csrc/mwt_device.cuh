@@ -170,21 +170,31 @@ struct Box {
 __device__ __forceinline__ Ray gen_ray(int mode, const Box &b, unsigned long long key,
                                        unsigned long long idx) {
     unsigned long long s0 = mix64(key ^ idx);
-    double x = 1.0, y = 0.0, r2 = 1.0;
-    bool ok = false;
-    for (int a = 0; a < 64; a++) {
-        x = 2.0 * u01(s0, 2 * a) - 1.0;
-        y = 2.0 * u01(s0, 2 * a + 1) - 1.0;
-        r2 = x * x + y * y;
-        if (r2 <= 1.0 && r2 > 0x1p-60) { ok = true; break; }
+    // unit-disk rejection: the first accepted attempt a in 0..63.  Attempts 0
+    // and 1 are evaluated unconditionally (accepted together with probability
+    // 1 - (1 - pi/4)^2 = 95%) so the warp stays converged; the rest is a rare loop.
+    const double xa = 2.0 * u01(s0, 0) - 1.0, ya = 2.0 * u01(s0, 1) - 1.0;
+    const double xb = 2.0 * u01(s0, 2) - 1.0, yb = 2.0 * u01(s0, 3) - 1.0;
+    const double ra = xa * xa + ya * ya, rb = xb * xb + yb * yb;
+    const bool oka = ra <= 1.0 && ra > 0x1p-60, okb = rb <= 1.0 && rb > 0x1p-60;
+    double x = oka ? xa : xb, y = oka ? ya : yb, r2 = oka ? ra : rb;
+    bool ok = oka || okb;
+    if (!ok) {
+        for (int a = 2; a < 64; a++) {
+            x = 2.0 * u01(s0, 2 * a) - 1.0;
+            y = 2.0 * u01(s0, 2 * a + 1) - 1.0;
+            r2 = x * x + y * y;
+            if (r2 <= 1.0 && r2 > 0x1p-60) {
+                ok = true;
+                break;
+            }
+        }
     }
     Ray r;
-    r.dx = 1.0;
-    r.dy = 0.0;
-    if (ok) {
-        double n = sqrt(r2);
-        r.dx = x / n;
-        r.dy = y / n;
+    {
+        const double n = sqrt(ok ? r2 : 1.0);
+        r.dx = ok ? x / n : 1.0;
+        r.dy = ok ? y / n : 0.0;
     }
     double W = b.x1 - b.x0, H = b.y1 - b.y0;
     if (mode == MWT_RAYS_INTERIOR) {
@@ -196,11 +206,12 @@ __device__ __forceinline__ Ray gen_ray(int mode, const Box &b, unsigned long lon
         double w = 0.5 * (fabs(nx) * W + fabs(ny) * H);
         double s = w * (2.0 * u01(s0, 128) - 1.0);
         double px = cx + s * nx, py = cy + s * ny;
-        double tx = -CUDART_INF, ty = -CUDART_INF;
-        if (r.dx > 0.0) tx = (b.x0 - px) / r.dx;
-        else if (r.dx < 0.0) tx = (b.x1 - px) / r.dx;
-        if (r.dy > 0.0) ty = (b.y0 - py) / r.dy;
-        else if (r.dy < 0.0) ty = (b.y1 - py) / r.dy;
+        // entry parameter per slab: (x0 - px)/dx if dx > 0, (x1 - px)/dx if dx < 0,
+        // -inf if dx == 0 (one division per axis, no divergence)
+        const double qx = (r.dx > 0.0 ? b.x0 : b.x1) - px;
+        const double qy = (r.dy > 0.0 ? b.y0 : b.y1) - py;
+        const double tx = r.dx != 0.0 ? qx / r.dx : -CUDART_INF;
+        const double ty = r.dy != 0.0 ? qy / r.dy : -CUDART_INF;
         if (tx >= ty) {
             r.ox = r.dx > 0.0 ? b.x0 : b.x1;
             double oy = py + tx * r.dy;

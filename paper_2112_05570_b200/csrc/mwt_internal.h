@@ -113,7 +113,7 @@ int launch_trace(const MeshDev &m, const double *rays, const int32_t *start, int
 int launch_trace_generated(const MeshDev &m, int mode, const double *box, uint64_t seed,
                            uint64_t first, int64_t n, int32_t *o_seg, double *o_t,
                            int32_t *o_steps, long long *hist, void *stream);
-void set_tuning(int refill_below, int min_blocks);
+void set_tuning(int refill_below, int min_blocks, int variant);
 int launch_histogram(const int32_t *seg, const int32_t *steps, const uint32_t *st, int64_t n,
                      long long *hist, void *stream);
 int launch_bvh(const MeshDev &m, const BvhDev &b, const double *rays, int64_t n, int32_t *o_seg,

@@ -140,38 +140,42 @@ __device__ __forceinline__ int locate(const MeshDev &M, double px, double py, ui
     const double sx = ((double)cx + 0.5) / dres, sy = ((double)cy + 0.5) / dres;
     const double dx = px - sx, dy = py - sy;
     int cur = __ldg(M.anchor + cy * res + cx);
-    int ent = -1;
     double e0, e1, e2;
-    bool found = false;
-    const int cap = 4 * M.nt + 16;
-    for (int it = 0; it < cap; it++) {
-        corners(M, cur, P0, P1, P2);
-        edge_areas(P0, P1, P2, px, py, e0, e1, e2);
-        if (inside(e0, e1, e2)) {
-            found = true;
-            break;
+    corners(M, cur, P0, P1, P2);
+    edge_areas(P0, P1, P2, px, py, e0, e1, e2);
+    if (!inside(e0, e1, e2)) {  // seed cell centre and p in different triangles
+        int ent = -1;
+        bool found = false;
+        const int cap = 4 * M.nt + 16;
+        for (int it = 0; it < cap; it++) {
+            // straight walk toward p, exit rule of accel.py:314-322
+            double s0 = dx * (P0.y - sy) - dy * (P0.x - sx);
+            double s1 = dx * (P1.y - sy) - dy * (P1.x - sx);
+            double s2 = dx * (P2.y - sy) - dy * (P2.x - sx);
+            int best = -1;
+            double bt = 0.0;
+            if (ent != 0 && s1 <= 0.0 && 0.0 <= s2 && s2 - s1 > bt) { bt = s2 - s1; best = 0; }
+            if (ent != 1 && s2 <= 0.0 && 0.0 <= s0 && s0 - s2 > bt) { bt = s0 - s2; best = 1; }
+            if (ent != 2 && s0 <= 0.0 && 0.0 <= s1 && s1 - s0 > bt) { bt = s1 - s0; best = 2; }
+            if (best < 0) break;
+            int word = (int)pick(__ldg(M.lnbr + cur), best);
+            if (word < 0) break;
+            cur = word >> 2;
+            ent = word & 3;
+            corners(M, cur, P0, P1, P2);
+            edge_areas(P0, P1, P2, px, py, e0, e1, e2);
+            if (inside(e0, e1, e2)) {
+                found = true;
+                break;
+            }
         }
-        // straight walk toward p, exit rule of accel.py:314-322
-        double s0 = dx * (P0.y - sy) - dy * (P0.x - sx);
-        double s1 = dx * (P1.y - sy) - dy * (P1.x - sx);
-        double s2 = dx * (P2.y - sy) - dy * (P2.x - sx);
-        int best = -1;
-        double bt = 0.0;
-        if (ent != 0 && s1 <= 0.0 && 0.0 <= s2 && s2 - s1 > bt) { bt = s2 - s1; best = 0; }
-        if (ent != 1 && s2 <= 0.0 && 0.0 <= s0 && s0 - s2 > bt) { bt = s0 - s2; best = 1; }
-        if (ent != 2 && s0 <= 0.0 && 0.0 <= s1 && s1 - s0 > bt) { bt = s1 - s0; best = 2; }
-        if (best < 0) break;
-        int word = (int)pick(__ldg(M.lnbr + cur), best);
-        if (word < 0) break;
-        cur = word >> 2;
-        ent = word & 3;
-    }
-    if (!found) {
-        const LocRes lr = loc_brute(M.cxy, M.nt, px, py);
-        st |= ST_LOC_BRUTE | lr.st;
-        cur = lr.tid;
-        corners(M, cur, P0, P1, P2);
-        edge_areas(P0, P1, P2, px, py, e0, e1, e2);
+        if (!found) {
+            const LocRes lr = loc_brute(M.cxy, M.nt, px, py);
+            st |= ST_LOC_BRUTE | lr.st;
+            cur = lr.tid;
+            corners(M, cur, P0, P1, P2);
+            edge_areas(P0, P1, P2, px, py, e0, e1, e2);
+        }
     }
     if (M.flood_filter && fabs(px) <= 4.0 && fabs(py) <= 4.0) {
         // only neighbours across edges with value <= 1e-12 can contain p; a
@@ -595,6 +599,152 @@ __global__ void __launch_bounds__(kThreads, MINB)
     if (hist) hist_flush(h, steps_sum, hist);
 }
 
+// ---------------------------------------------------------------------------
+// Queue variant (default).  Each warp keeps two 32-entry lane-state queues in
+// shared memory.  Prologues run in bulk -- all 32 lanes prepare the next 32
+// rays of the warp's chunk (raygen / load, locate, first triangle) into the
+// prologue queue -- and walking lanes that go idle pop a prepared ray every
+// iteration, so walk steps run with nearly all lanes busy.  Rays that reach
+// their exit edge park in the epilogue queue; when it would overflow, all
+// lanes resolve the parked rays together (hit test, canonical, writes).
+
+struct LaneQ {  // SoA, one entry per lane slot
+    double ox[32], oy[32], dx[32], dy[32], sp[32], sq[32];
+    long long idx[32];
+    uint32_t w[32], st[32];
+    int cur[32], ei[32], steps[32];
+    unsigned char phase[32], fast[32];
+};
+
+template <bool GEN, int MINB>
+__global__ void __launch_bounds__(kThreads, MINB)
+    k_trace_q(MeshDev M, RaySrc src, long long n, TraceOut out, long long *hist) {
+    __shared__ unsigned int h[MWT_HIST_LEN];
+    __shared__ LaneQ qs[2 * (kThreads / 32)];
+    if (hist) hist_init(h);
+    const unsigned FULL = 0xffffffffu;
+    const int lane = threadIdx.x & 31;
+    const unsigned lt_mask = (1u << lane) - 1u;
+    LaneQ &PQ = qs[2 * (threadIdx.x >> 5)];
+    LaneQ &EQ = qs[2 * (threadIdx.x >> 5) + 1];
+    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
+    const long long chunk = (n + nwarps - 1) / nwarps;
+    long long next = warp * chunk;
+    const long long end = next + chunk < n ? next + chunk : n;
+    unsigned long long steps_sum = 0;
+    int pro_h = 0, pro_n = 0, epi_n = 0;  // warp-uniform queue cursors
+
+    int phase = 0;  // 0 idle, 1 walking, 2 exit edge reached, 3 failed
+    long long idx = 0;
+    Ray r;
+    WalkState s;
+    uint32_t st = 0;
+
+    // all lanes: resolve the first cnt parked rays of EQ
+    auto bulk_epilogue = [&](int cnt) {
+        if (lane < cnt) {
+            const int k = lane;
+            const int seg0 = -1;
+            int seg = seg0;
+            double t = CUDART_NAN, u = CUDART_NAN;
+            uint32_t est = EQ.st[k];
+            if (EQ.phase[k] == 2) {
+                const Term tm = terminal(M.seg, M.ep_range, M.ep_ids, M.cxy, EQ.ox[k], EQ.oy[k],
+                                         EQ.dx[k], EQ.dy[k], EQ.cur[k], EQ.ei[k], EQ.w[k], EQ.sp[k],
+                                         EQ.sq[k], est);
+                seg = tm.seg;
+                t = tm.t;
+                u = tm.u;
+                est = tm.st;
+            }
+            const long long q = EQ.idx[k];
+            const int nst = EQ.steps[k];
+            if (out.seg) out.seg[q] = seg;
+            if (out.t) out.t[q] = t;
+            if (out.u) out.u[q] = u;
+            if (out.steps) out.steps[q] = nst;
+            if (out.st) out.st[q] = est;
+            if (hist) {
+                hist_add(h, seg, nst, est);
+                steps_sum += (unsigned long long)nst;
+            }
+        }
+        __syncwarp();
+    };
+
+    while (true) {
+        // parked lanes -> epilogue queue
+        const unsigned pend = __ballot_sync(FULL, phase >= 2);
+        if (pend) {
+            if (epi_n + __popc(pend) > 32) {
+                bulk_epilogue(epi_n);
+                epi_n = 0;
+            }
+            if (phase >= 2) {
+                const int k = epi_n + __popc(pend & lt_mask);
+                EQ.ox[k] = r.ox; EQ.oy[k] = r.oy; EQ.dx[k] = r.dx; EQ.dy[k] = r.dy;
+                EQ.sp[k] = s.sp; EQ.sq[k] = s.sq; EQ.idx[k] = idx; EQ.w[k] = s.w; EQ.st[k] = st;
+                EQ.cur[k] = s.cur; EQ.ei[k] = s.ei; EQ.steps[k] = s.steps;
+                EQ.phase[k] = (unsigned char)phase;
+                phase = 0;
+            }
+            epi_n += __popc(pend);
+            __syncwarp();
+        }
+        // idle lanes <- prologue queue (bulk refill when exhausted)
+        const unsigned idle = __ballot_sync(FULL, phase == 0);
+        if (idle) {
+            if (pro_h == pro_n && next < end) {
+                const long long i = next + lane;
+                if (i < end) {
+                    const Init in = prologue<GEN>(
+                        i, src.mode, src.box.x0, src.box.y0, src.box.x1, src.box.y1, src.key,
+                        src.first, src.rays, src.start, M.nt, M.res, M.flood_filter, M.cxy, M.lnbr,
+                        M.link, M.anchor);
+                    PQ.ox[lane] = in.ox; PQ.oy[lane] = in.oy; PQ.dx[lane] = in.dx; PQ.dy[lane] = in.dy;
+                    PQ.sp[lane] = in.sp; PQ.sq[lane] = in.sq; PQ.idx[lane] = i; PQ.w[lane] = in.w;
+                    PQ.st[lane] = in.st; PQ.cur[lane] = in.cur; PQ.ei[lane] = in.ei;
+                    PQ.steps[lane] = in.steps; PQ.phase[lane] = (unsigned char)in.phase;
+                    PQ.fast[lane] = in.fast ? 1 : 0;
+                    if (out.start) out.start[i] = in.start;
+                }
+                pro_h = 0;
+                pro_n = end - next < 32 ? (int)(end - next) : 32;
+                next += pro_n;
+                __syncwarp();
+            }
+            const int avail = pro_n - pro_h;
+            if (phase == 0) {
+                const int rank = __popc(idle & lt_mask);
+                if (rank < avail) {
+                    const int k = pro_h + rank;
+                    r.ox = PQ.ox[k]; r.oy = PQ.oy[k]; r.dx = PQ.dx[k]; r.dy = PQ.dy[k];
+                    s.sp = PQ.sp[k]; s.sq = PQ.sq[k]; idx = PQ.idx[k]; s.w = PQ.w[k]; st = PQ.st[k];
+                    s.cur = PQ.cur[k]; s.ei = PQ.ei[k]; s.steps = PQ.steps[k];
+                    s.fast = PQ.fast[k] != 0;
+                    phase = PQ.phase[k];
+                }
+            }
+            const int took = __popc(idle) < avail ? __popc(idle) : avail;
+            pro_h += took;
+        }
+        const unsigned walking = __ballot_sync(FULL, phase == 1);
+        if (walking == 0) {
+            if (next >= end && pro_h == pro_n && __ballot_sync(FULL, phase != 0) == 0) {
+                if (epi_n) bulk_epilogue(epi_n);
+                break;
+            }
+            continue;
+        }
+        if (phase == 1) {
+            if (!walk_step(M, r, s, st)) phase = 3;
+            else if (s.w & kStopBit) phase = 2;
+        }
+    }
+    if (hist) hist_flush(h, steps_sum, hist);
+}
+
 __global__ void __launch_bounds__(kThreads) k_raygen(int mode, Box box, unsigned long long key,
                                                      unsigned long long first, long long n,
                                                      double *rays) {
@@ -640,30 +790,34 @@ __global__ void __launch_bounds__(kThreads) k_histogram(const int32_t *seg, cons
 
 #define MWT_LAUNCH_RET return (int)cudaGetLastError()
 
-static int g_refill_below = 16;
-static int g_min_blocks = 4;  // 4: <= 64 regs (32 warps/SM); 3: <= 80 regs (24 warps/SM)
+static int g_refill_below = 4;  // tuned on B200 (tools/tune.py): refill late, walk long
+static int g_min_blocks = 3;   // 3: <= 80 regs (24 warps/SM), the measured best; 4: 64 regs; 2: no cap
 
-template <bool GEN, int MINB>
-static int persistent_grid(long long n) {
-    static int blocks_per_sm = 0, sms = 0;
-    if (blocks_per_sm == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_trace<GEN, MINB>, kThreads, 0);
-        if (blocks_per_sm <= 0) blocks_per_sm = 1;
-        if (sms <= 0) sms = 148;
-    }
+static int g_variant = 1;      // 1: refill kernel (k_trace, measured faster); 0: queue kernel (k_trace_q)
+
+template <typename K>
+static int persistent_grid(K kernel, long long n) {
+    int dev = 0, sms = 0, blocks_per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kernel, kThreads, 0);
+    if (blocks_per_sm <= 0) blocks_per_sm = 1;
+    if (sms <= 0) sms = 148;
     long long want = (n + kThreads - 1) / kThreads;
-    long long cap = (long long)sms * blocks_per_sm;
+    long long cap = (long long)sms * blocks_per_sm;  // one resident wave
     return (int)(want < cap ? (want < 1 ? 1 : want) : cap);
 }
 
 template <bool GEN, int MINB>
 static void launch_k_trace(const MeshDev &m, const RaySrc &src, long long n, const TraceOut &out,
                            long long *hist, void *stream) {
-    k_trace<GEN, MINB><<<persistent_grid<GEN, MINB>(n), kThreads, 0, (cudaStream_t)stream>>>(
-        m, src, n, out, hist, g_refill_below);
+    if (g_variant == 1) {
+        k_trace<GEN, MINB><<<persistent_grid(k_trace<GEN, MINB>, n), kThreads, 0,
+                             (cudaStream_t)stream>>>(m, src, n, out, hist, g_refill_below);
+    } else {
+        k_trace_q<GEN, MINB><<<persistent_grid(k_trace_q<GEN, MINB>, n), kThreads, 0,
+                               (cudaStream_t)stream>>>(m, src, n, out, hist);
+    }
 }
 
 template <bool GEN>
@@ -726,9 +880,10 @@ int launch_histogram(const int32_t *seg, const int32_t *steps, const uint32_t *s
     MWT_LAUNCH_RET;
 }
 
-void set_tuning(int refill_below, int min_blocks) {
+void set_tuning(int refill_below, int min_blocks, int variant) {
     if (refill_below >= 0) g_refill_below = refill_below > 31 ? 31 : refill_below;
     if (min_blocks >= 2 && min_blocks <= 4) g_min_blocks = min_blocks;
+    if (variant == 0 || variant == 1) g_variant = variant;
 }
 
 }  // namespace mwt

@@ -102,8 +102,8 @@ def test_generated_kernel_equals_explicit_rays_and_histogram():
         assert np.array_equal(h2.cpu().numpy(), ref)
 
 
-@pytest.mark.parametrize("refill,minb", [(0, 4), (4, 3), (16, 2), (31, 4)])
-def test_tuning_knobs_do_not_change_results(refill, minb):
+@pytest.mark.parametrize("refill,minb,variant", [(0, 4, 1), (4, 3, 1), (16, 2, 1), (31, 4, 1), (0, 4, 0), (0, 3, 0), (0, 2, 0)])
+def test_tuning_knobs_do_not_change_results(refill, minb, variant):
     from oracle import oracle as orc
     from paper_2112_05570_b200 import _lib
     from paper_2112_05570_b200.engine import DeviceMesh
@@ -111,11 +111,11 @@ def test_tuning_knobs_do_not_change_results(refill, minb):
     m, om = DeviceMesh.from_files(*paths), orc.Mesh.from_files(*paths)
     rays = orc.raygen(0, (0, 0, 1, 1), 2, 0, 50000)
     ref = om.trace(rays)
-    _lib.check(_lib.lib.mwt_set_tuning(refill, minb))
+    _lib.check(_lib.lib.mwt_set_tuning(refill, minb, variant))
     try:
         got = m.trace(rays)
     finally:
-        _lib.lib.mwt_set_tuning(16, 4)
+        _lib.lib.mwt_set_tuning(4, 3, 1)
     for k in ("start", "seg", "steps"):
         assert np.array_equal(got[k], ref[k])
 

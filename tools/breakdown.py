@@ -17,7 +17,7 @@ box = (0.0, 0.0, 1.0, 0.5) if cfg == "grass4096" else (0.0, 0.0, 1.0, 1.0)
 d = os.path.join(ROOT, "fixtures", "data", cfg)
 mesh = DeviceMesh.from_files(os.path.join(d, "scene.txt"), os.path.join(d, f"{which}.tri"))
 if len(sys.argv) > 4:
-    _lib.lib.mwt_set_tuning(int(sys.argv[3]), int(sys.argv[4]))
+    _lib.lib.mwt_set_tuning(int(sys.argv[3]), int(sys.argv[4]), int(sys.argv[5]) if len(sys.argv) > 5 else 0)
 
 
 def timeit(fn, reps=5):

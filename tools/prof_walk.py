@@ -14,7 +14,7 @@ refill, minb = int(sys.argv[5]), int(sys.argv[6])
 box = (0.0, 0.0, 1.0, 0.5) if cfg == "grass4096" else (0.0, 0.0, 1.0, 1.0)
 d = os.path.join(ROOT, "fixtures", "data", cfg)
 mesh = DeviceMesh.from_files(os.path.join(d, "scene.txt"), os.path.join(d, f"{which}.tri"))
-_lib.check(_lib.lib.mwt_set_tuning(refill, minb))
+_lib.check(_lib.lib.mwt_set_tuning(refill, minb, int(os.environ.get("MWT_VARIANT", "0"))))
 rays = mesh.raygen_device(mode, box, 0, 0, n)
 tid, _ = mesh.locate_device(rays[:, :2].contiguous())
 for _ in range(4):

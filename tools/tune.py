@@ -21,9 +21,10 @@ if not os.path.exists(os.path.join(d, f"{which}.tri")):
 mesh = DeviceMesh.from_files(os.path.join(d, "scene.txt"), os.path.join(d, f"{which}.tri"))
 hist = new_histogram()
 res = []
-for minb in (2, 3, 4):
-    for refill in (4, 8, 12, 16):
-        _lib.lib.mwt_set_tuning(refill, minb)
+combos = [(0, m, 0) for m in (2, 3, 4)] + [(r, m, 1) for m in (2, 3) for r in (4, 8)]
+for refill, minb, variant in combos:
+    if True:
+        _lib.lib.mwt_set_tuning(refill, minb, variant)
         for mode in (0, 1):
             for _ in range(3):
                 mesh.trace_generated_device(mode, box, 0, 0, n, outputs=True, hist=hist)
@@ -39,7 +40,7 @@ for minb in (2, 3, 4):
                 times.append(e0.elapsed_time(e1))
             h = summarize_histogram(hist)
             ms = float(np.median(times))
-            res.append(dict(minb=minb, refill=refill, mode=mode, ms=ms, grays=n / ms / 1e6,
+            res.append(dict(variant=variant, minb=minb, refill=refill, mode=mode, ms=ms, grays=n / ms / 1e6,
                             steps=h["steps_per_ray"], gbs=h["steps_sum"] * 32 / ms / 1e6))
             print(json.dumps(res[-1]), flush=True)
-_lib.lib.mwt_set_tuning(16, 4)
+_lib.lib.mwt_set_tuning(4, 3, 1)
