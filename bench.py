@@ -170,7 +170,7 @@ def run_reference_arm(args, rank: int):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="engine", choices=["engine", "reference"])
     ap.add_argument("--config", default="lines1024", choices=sorted(CONFIGS))
@@ -272,6 +272,11 @@ def main():
     algo_bytes = hb["steps_sum"] * ALGO_BYTES_PER_STEP
     peak, peak_src = peaks()
     achieved = algo_bytes / (kms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as fh:
+            traffic = json.load(fh).get(f"{args.config}/{args.mesh}", {}).get("dram_bytes_per_launch")
 
     line = {
         "metric": "rays_per_s_mwt_walk", "value": value, "unit": "rays/s", "n_gpus": world,
@@ -287,10 +292,10 @@ def main():
                    "hit_fraction": hsum["hits"] / max(1, hsum["rays"])},
         "gpu_launches": len(parts) * args.steps,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
-                     "kernel": "k_trace_generated", "kernel_ms": kms,
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel": "k_trace (mwt_trace_generated_dev, box-entry launch)", "kernel_ms": kms,
                      "algo_bytes_per_launch": algo_bytes,
-                     "algo_bytes_rule": "32 B per triangle step (16-B link + 16-B apex corner)",
+                     "algo_bytes_rule": "32 B per triangle step (one 32-B step record: 2 exit words + apex corner)",
                      "peak_source": peak_src, "mesh_resident": "L2 (126 MB); HBM carries only per-ray output"},
         "histogram": {k: hsum[k] for k in ("rays", "hits", "misses", "steps_sum", "status")},
     }
