@@ -54,6 +54,7 @@ extern "C" {
 #define MWT_ST_LOC_BRUTE 256u  /* anchor walk failed, brute-force scan (accel.py:287-288) */
 #define MWT_ST_LOC_OUTSIDE 512u /* point outside every triangle: nearest centroid (accel.py:245-246) */
 #define MWT_ST_OVERFLOW 1024u  /* device capacity exceeded (flood/stack); result invalid */
+#define MWT_ST_BOUNDARY 2048u  /* engine-side note: start triangle from the boundary-edge table */
 
 /* ray generator modes (engine-defined) */
 #define MWT_RAYS_BOX_ENTRY 0   /* isotropic lines through the box, origin at box entry */
@@ -64,7 +65,7 @@ extern "C" {
 #define MWT_HIST_HIT 1024       /* rays with a hit */
 #define MWT_HIST_MISS 1025      /* rays without a hit (boundary / open edge) */
 #define MWT_HIST_STEPS_SUM 1026 /* sum of tri_steps */
-#define MWT_HIST_STATUS0 1027   /* 11 counters, one per MWT_ST_* bit */
+#define MWT_HIST_STATUS0 1027   /* 12 counters, one per MWT_ST_* bit */
 #define MWT_HIST_LEN 1040       /* int64 entries */
 
 typedef struct mwt_mesh mwt_mesh;

@@ -153,16 +153,18 @@ void orc_raygen_one(int mode, const double box[4], uint64_t key, uint64_t idx, d
     double x = 1.0, y = 0.0, r2 = 1.0;
     int ok = 0;
     for (int a = 0; a < 64; a++) {
-        x = 2.0 * u01(s0, 2 * a) - 1.0;
-        y = 2.0 * u01(s0, 2 * a + 1) - 1.0;
+        /* one 64-bit draw per attempt -> two 32-bit coordinates in [-1, 1) */
+        uint64_t z = mix64(s0 + (uint64_t)(a + 1) * GOLDEN);
+        x = 2.0 * ((double)(uint32_t)(z >> 32) * 0x1p-32) - 1.0;
+        y = 2.0 * ((double)(uint32_t)(z & 0xffffffffull) * 0x1p-32) - 1.0;
         r2 = x * x + y * y;
         if (r2 <= 1.0 && r2 > 0x1p-60) { ok = 1; break; }
     }
     double dx = 1.0, dy = 0.0;
     if (ok) {
-        double n = sqrt(r2);
-        dx = x / n;
-        dy = y / n;
+        double inv = 1.0 / sqrt(r2);
+        dx = x * inv;
+        dy = y * inv;
     }
     double x0 = box[0], y0 = box[1], x1 = box[2], y1 = box[3];
     double W = x1 - x0, H = y1 - y0;

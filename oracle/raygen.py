@@ -63,8 +63,11 @@ def raygen(mode: int, box, seed: int, first: int, n: int) -> np.ndarray:
         todo = ~ok
         if not todo.any():
             break
-        xa = 2.0 * _u01(s0[todo], 2 * a) - 1.0
-        ya = 2.0 * _u01(s0[todo], 2 * a + 1) - 1.0
+        with np.errstate(over="ignore"):
+            z = _mix(s0[todo] + np.uint64(a + 1) * GOLDEN)
+        # one 64-bit draw per attempt -> two 32-bit coordinates in [-1, 1)
+        xa = 2.0 * ((z >> np.uint64(32)).astype(np.float64) * 2.0 ** -32) - 1.0
+        ya = 2.0 * ((z & np.uint64(0xFFFFFFFF)).astype(np.float64) * 2.0 ** -32) - 1.0
         ra = xa * xa + ya * ya
         acc = (ra <= 1.0) & (ra > 2.0 ** -60)
         sel = np.nonzero(todo)[0]
@@ -72,9 +75,9 @@ def raygen(mode: int, box, seed: int, first: int, n: int) -> np.ndarray:
         y[sel] = ya
         r2[sel] = ra
         ok[sel[acc]] = True
-    nrm = np.sqrt(r2)
-    dx = np.where(ok, x / nrm, 1.0)
-    dy = np.where(ok, y / nrm, 0.0)
+    inv = 1.0 / np.sqrt(r2)
+    dx = np.where(ok, x * inv, 1.0)
+    dy = np.where(ok, y * inv, 0.0)
     x0, y0, x1, y1 = (float(v) for v in box)
     W, H = x1 - x0, y1 - y0
     if mode == MODE_INTERIOR:

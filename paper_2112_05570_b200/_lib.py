@@ -25,8 +25,11 @@ ST_LOC_TIE = 128
 ST_LOC_BRUTE = 256
 ST_LOC_OUTSIDE = 512
 ST_OVERFLOW = 1024
+ST_BOUNDARY = 2048
+# bits the engine sets about its own strategy (not reference semantics)
+ST_ENGINE_ONLY = ST_LOC_BRUTE | ST_BOUNDARY
 STATUS_NAMES = ("error", "fallback", "grazing", "canonical", "parallel", "zero_side", "multi",
-                "locate_tie", "locate_brute", "locate_outside", "overflow")
+                "locate_tie", "locate_brute", "locate_outside", "overflow", "boundary_start")
 
 RAYS_BOX_ENTRY = 0
 RAYS_INTERIOR = 1

@@ -117,7 +117,10 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     size_t bytes = Arena::align(nt * 16) + Arena::align(nt * 48) + Arena::align(nt * 16) +
                    Arena::align(nt * 96) +
                    Arena::align(ns * 32) + Arena::align(ns) + Arena::align(ns * 2 * 8) +
-                   Arena::align(P.ep_ids.size() * 4) + Arena::align(P.anchor.size() * 4);
+                   Arena::align(P.ep_ids.size() * 4) + Arena::align(P.anchor.size() * 4) +
+                   Arena::align(P.bu.size() * 8) + Arena::align(P.bpq.size() * 8) +
+                   Arena::align(P.bword.size() * 4) + Arena::align(P.bbucket.size() * 4) +
+                   Arena::align(sizeof(mwt::MeshDev));
     Arena a;
     CK(cudaMalloc(&a.base, bytes));
     a.size = bytes;
@@ -133,6 +136,11 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     int2 *epr = carve<int2>(a, 2 * ns);
     int32_t *epi = carve<int32_t>(a, P.ep_ids.size());
     int32_t *anc = carve<int32_t>(a, P.anchor.size());
+    double *bu = carve<double>(a, P.bu.size());
+    double *bpq = carve<double>(a, P.bpq.size());
+    int32_t *bword = carve<int32_t>(a, P.bword.size());
+    int32_t *bbucket = carve<int32_t>(a, P.bbucket.size());
+    mwt::MeshDev *self = carve<mwt::MeshDev>(a, 1);
     cudaError_t e = cudaSuccess;
     auto up = [&](void *dst, const void *src, size_t n) {
         if (e == cudaSuccess && n) e = cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
@@ -146,13 +154,37 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     up(epr, P.ep_range.data(), (size_t)P.ns * 16);
     up(epi, P.ep_ids.data(), P.ep_ids.size() * 4);
     up(anc, P.anchor.data(), P.anchor.size() * 4);
+    up(bu, P.bu.data(), P.bu.size() * 8);
+    up(bpq, P.bpq.data(), P.bpq.size() * 8);
+    up(bword, P.bword.data(), P.bword.size() * 4);
+    up(bbucket, P.bbucket.data(), P.bbucket.size() * 4);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         cudaFree(a.base);
         delete m;
         return cuda_fail(e, "mesh_create: upload");
     }
-    m->dev = mwt::MeshDev{P.nt, P.ns, P.res, P.flood_filter, link, cxy, step, lnbr, seg, kind, epr, epi, anc};
+    m->dev = mwt::MeshDev{P.nt, P.ns, P.res, P.flood_filter, link, cxy, step, lnbr, seg, kind, epr, epi, anc,
+                         P.res > 0 ? 1.0 / P.res : 0.0};
+    m->dev.nbsides = P.nbsides;
+    for (int k = 0; k < P.nbsides; k++) {
+        const auto &S = P.sides[k];
+        m->dev.bs[k] = mwt::MeshDev::BSide{S.axis, S.off, S.cnt, S.boff, S.nb, S.c, S.lo, S.hi, S.scale};
+    }
+    m->dev.bu = reinterpret_cast<const double2 *>(bu);
+    m->dev.bpq = reinterpret_cast<const double4 *>(bpq);
+    m->dev.bword = bword;
+    m->dev.bbucket = bbucket;
+    m->dev.self = self;
+    {
+        cudaError_t e2 = cudaMemcpy(self, &m->dev, sizeof(mwt::MeshDev), cudaMemcpyHostToDevice);
+        if (e2 != cudaSuccess) {
+            cudaStreamDestroy(m->stream);
+            cudaFree(a.base);
+            delete m;
+            return cuda_fail(e2, "mesh_create: descriptor upload");
+        }
+    }
     m->info.num_vertices = P.nv;
     m->info.num_triangles = P.nt;
     m->info.num_segments = P.ns;

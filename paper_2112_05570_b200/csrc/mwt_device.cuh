@@ -159,8 +159,18 @@ static inline unsigned long long ray_key(unsigned long long seed, unsigned long 
     return mix64(mix64(seed + kGolden) ^ (stream * 0xD1B54A32D192ED03ull));
 }
 
+// draw k of ray state s0: 53-bit uniform in [0, 1)
 __device__ __forceinline__ double u01(unsigned long long s0, unsigned long long k) {
     return (double)(mix64(s0 + (k + 1ull) * kGolden) >> 11) * 0x1p-53;
+}
+
+// rejection attempt a: one 64-bit draw -> two 32-bit coordinates in [-1, 1)
+__device__ __forceinline__ void disk_try(unsigned long long s0, int a, double &x, double &y,
+                                         double &r2) {
+    const unsigned long long z = mix64(s0 + (unsigned long long)(a + 1) * kGolden);
+    x = 2.0 * ((double)(unsigned)(z >> 32) * 0x1p-32) - 1.0;
+    y = 2.0 * ((double)(unsigned)(z & 0xffffffffull) * 0x1p-32) - 1.0;
+    r2 = x * x + y * y;
 }
 
 struct Box {
@@ -173,17 +183,15 @@ __device__ __forceinline__ Ray gen_ray(int mode, const Box &b, unsigned long lon
     // unit-disk rejection: the first accepted attempt a in 0..63.  Attempts 0
     // and 1 are evaluated unconditionally (accepted together with probability
     // 1 - (1 - pi/4)^2 = 95%) so the warp stays converged; the rest is a rare loop.
-    const double xa = 2.0 * u01(s0, 0) - 1.0, ya = 2.0 * u01(s0, 1) - 1.0;
-    const double xb = 2.0 * u01(s0, 2) - 1.0, yb = 2.0 * u01(s0, 3) - 1.0;
-    const double ra = xa * xa + ya * ya, rb = xb * xb + yb * yb;
+    double xa, ya, ra, xb, yb, rb;
+    disk_try(s0, 0, xa, ya, ra);
+    disk_try(s0, 1, xb, yb, rb);
     const bool oka = ra <= 1.0 && ra > 0x1p-60, okb = rb <= 1.0 && rb > 0x1p-60;
     double x = oka ? xa : xb, y = oka ? ya : yb, r2 = oka ? ra : rb;
     bool ok = oka || okb;
     if (!ok) {
         for (int a = 2; a < 64; a++) {
-            x = 2.0 * u01(s0, 2 * a) - 1.0;
-            y = 2.0 * u01(s0, 2 * a + 1) - 1.0;
-            r2 = x * x + y * y;
+            disk_try(s0, a, x, y, r2);
             if (r2 <= 1.0 && r2 > 0x1p-60) {
                 ok = true;
                 break;
@@ -192,9 +200,9 @@ __device__ __forceinline__ Ray gen_ray(int mode, const Box &b, unsigned long lon
     }
     Ray r;
     {
-        const double n = sqrt(ok ? r2 : 1.0);
-        r.dx = ok ? x / n : 1.0;
-        r.dy = ok ? y / n : 0.0;
+        const double inv = 1.0 / sqrt(ok ? r2 : 1.0);
+        r.dx = ok ? x * inv : 1.0;
+        r.dy = ok ? y * inv : 0.0;
     }
     double W = b.x1 - b.x0, H = b.y1 - b.y0;
     if (mode == MWT_RAYS_INTERIOR) {

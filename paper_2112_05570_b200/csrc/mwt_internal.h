@@ -60,6 +60,19 @@ struct HostPacked {
     std::vector<int32_t> ep_range;  // 2*(2*ns)
     std::vector<int32_t> ep_ids;
     std::vector<int32_t> anchor;    // res*res
+    // boundary-edge table (box-entry start triangles), one side per boundary segment
+    int32_t nbsides = 0;
+    struct Side {
+        int32_t axis;      // 0: side lies on y = c (u = x); 1: on x = c (u = y)
+        double c, lo, hi;  // the line, and the side's u extent
+        int32_t off, cnt;  // its edges in bedge order (sorted by umin)
+        int32_t boff, nb;  // its buckets
+        double scale;      // nb / (hi - lo)
+    } sides[4];
+    std::vector<double> bu;         // 2 per edge: umin, umax
+    std::vector<double> bpq;        // 4 per edge: P (corner (j+1)%3), Q (corner (j+2)%3)
+    std::vector<int32_t> bword;     // (T << 2) | j, j = the boundary edge's index in T
+    std::vector<int32_t> bbucket;   // first edge (side-local) whose umax > bucket start
 };
 
 // Build the packed layout; returns MWT_OK or an error code with *err set.
@@ -80,6 +93,21 @@ struct MeshDev {
     const int2 *ep_range;
     const int32_t *ep_ids;
     const int32_t *anchor;
+    double inv_res;  // 1.0 / res (seed-cell centres: (c + 0.5) * inv_res)
+    // boundary-edge table: start triangles of rays whose origin lies on a box side
+    int32_t nbsides;
+    struct BSide {
+        int32_t axis, off, cnt, boff, nb;
+        double c, lo, hi, scale;
+    } bs[4];
+    const double2 *bu;      // (umin, umax) per edge
+    const double4 *bpq;     // (P.x, P.y, Q.x, Q.y) per edge
+    const int32_t *bword;
+    const int32_t *bbucket;
+    // a device-memory copy of this struct, for out-of-line device functions
+    // (passing the kernel-parameter copy by reference would force it into
+    // local memory)
+    const MeshDev *self;
 };
 
 struct BvhDev {

@@ -180,6 +180,74 @@ int pack_mesh(const double *vx, const double *vy, int32_t nv, const int32_t *tv,
     }
     if (P.ep_ids.empty()) P.ep_ids.push_back(0);
 
+    // boundary-edge table: for each axis-aligned boundary segment (a side of
+    // the square), its constrained mesh edges sorted along the side, with the
+    // triangle they bound and a bucket index for O(1) lookup
+    P.nbsides = 0;
+    for (int f = 0; f < ns && P.nbsides < 4; f++) {
+        if (seg_kind[f] == 0) continue;
+        const double ax = seg_xy[4LL * f], ay = seg_xy[4LL * f + 1];
+        const double bx = seg_xy[4LL * f + 2], by = seg_xy[4LL * f + 3];
+        int axis;
+        if (ay == by) axis = 0;       // horizontal: u = x
+        else if (ax == bx) axis = 1;  // vertical: u = y
+        else continue;
+        struct E {
+            double umin, umax, px, py, qx, qy;
+            int32_t word;
+        };
+        std::vector<E> es;
+        bool ok = true;
+        for (int t = 0; t < nt && ok; t++)
+            for (int i = 0; i < 3; i++) {
+                if (tf[3 * t + i] != f) continue;
+                const int a = tv[3 * t + (i + 1) % 3], b = tv[3 * t + (i + 2) % 3];
+                // endpoints may sit a rounding off the side line (the CDT splits
+                // boundary edges at points within its tolerance); the device
+                // tests containment with the actual coordinates
+                const double ua = axis == 0 ? vx[a] : vy[a], ub = axis == 0 ? vx[b] : vy[b];
+                es.push_back({std::min(ua, ub), std::max(ua, ub), vx[a], vy[a], vx[b], vy[b],
+                              (int32_t)(((uint32_t)t << 2) | (uint32_t)i)});
+            }
+        if (!ok || es.empty()) continue;
+        std::sort(es.begin(), es.end(), [](const E &p, const E &q) { return p.umin < q.umin; });
+        bool tiled = true;  // the edges must tile the side without gaps or overlaps
+        for (size_t k = 1; k < es.size(); k++)
+            if (es[k].umin != es[k - 1].umax) tiled = false;
+        if (!tiled) continue;
+        HostPacked::Side &S = P.sides[P.nbsides++];
+        S.axis = axis;
+        S.c = axis == 0 ? ay : ax;
+        S.lo = es.front().umin;
+        S.hi = es.back().umax;
+        S.off = (int32_t)P.bword.size();
+        S.cnt = (int32_t)es.size();
+        S.nb = 8 * S.cnt;
+        S.scale = S.nb / (S.hi - S.lo);
+        S.boff = (int32_t)P.bbucket.size();
+        for (const E &e : es) {
+            P.bu.push_back(e.umin);
+            P.bu.push_back(e.umax);
+            P.bpq.push_back(e.px);
+            P.bpq.push_back(e.py);
+            P.bpq.push_back(e.qx);
+            P.bpq.push_back(e.qy);
+            P.bword.push_back(e.word);
+        }
+        int k = 0;
+        for (int b = 0; b < S.nb; b++) {
+            const double start = S.lo + b / S.scale;
+            while (k < S.cnt - 1 && es[k].umax <= start) k++;
+            P.bbucket.push_back(k);
+        }
+    }
+    if (P.bword.empty()) {  // keep device pointers valid
+        P.bu.assign(2, 0.0);
+        P.bpq.assign(4, 0.0);
+        P.bword.assign(1, 0);
+        P.bbucket.assign(1, 0);
+    }
+
     if (nt == 0) {  // scene-only mesh (BVH / kd / brute force); no walk, no locate
         P.res = 0;
         P.anchor.assign(1, 0);
@@ -203,7 +271,8 @@ int pack_mesh(const double *vx, const double *vy, int32_t nv, const int32_t *tv,
     int hint = -1;
     for (int cy = 0; cy < res; cy++)
         for (int cx = 0; cx < res; cx++) {
-            double px = (cx + 0.5) / res, py = (cy + 0.5) / res;
+            const double inv = 1.0 / res;  // the device seeds walks from the same points
+            double px = (cx + 0.5) * inv, py = (cy + 0.5) * inv;
             bool strict = false;
             int tid = tri_locate(c, px, py, hint, &strict);
             if (!strict) P.anchors_not_strict++;

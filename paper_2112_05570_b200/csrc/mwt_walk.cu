@@ -137,7 +137,8 @@ __device__ __forceinline__ int locate(const MeshDev &M, double px, double py, ui
     int cy = vy < 0.0 ? 0 : (vy >= dres ? res - 1 : (int)vy);
     if (!(vx == vx)) cx = 0;
     if (!(vy == vy)) cy = 0;
-    const double sx = ((double)cx + 0.5) / dres, sy = ((double)cy + 0.5) / dres;
+    // seed point: the centre of the cell, computed exactly as the packer did
+    const double sx = ((double)cx + 0.5) * M.inv_res, sy = ((double)cy + 0.5) * M.inv_res;
     const double dx = px - sx, dy = py - sy;
     int cur = __ldg(M.anchor + cy * res + cx);
     double e0, e1, e2;
@@ -413,7 +414,7 @@ __device__ __forceinline__ void hist_add(unsigned int *h, int seg, int steps, ui
     atomicAdd(h + bin, 1u);
     atomicAdd(h + (seg >= 0 ? MWT_HIST_HIT : MWT_HIST_MISS), 1u);
     if (st) {
-        for (int b = 0; b < 11; b++)
+        for (int b = 0; b < 12; b++)
             if (st & (1u << b)) atomicAdd(h + MWT_HIST_STATUS0 + b, 1u);
     }
 }
@@ -456,20 +457,57 @@ struct Init {
     bool fast;
 };
 
+// Box-entry start: for a ray whose origin lies on a side of the square, the
+// boundary-edge table gives the triangle T bounded there.  If T is provably
+// the ONLY triangle that _contains the origin (accel.py:219-223; the two other
+// edge values exceed the flood bound of 1e-12), T is the reference's start
+// triangle (accel.py:226-238), and if the edge's endpoints straddle the ray
+// (side(Q) < 0 < side(P)) the first-triangle scan of accel.py:171-191 reduces
+// to an ordinary step entered through that edge: it is no candidate (sp > 0)
+// and has trans < 0, so neither the exit nor the fallback choice can pick it.
+__device__ __forceinline__ bool boundary_start(const MeshDev &M, const Ray &r, WalkState &s) {
+    if (!(M.flood_filter && fabs(r.ox) <= 4.0 && fabs(r.oy) <= 4.0)) return false;
+    for (int k = 0; k < M.nbsides; k++) {
+        const MeshDev::BSide &S = M.bs[k];
+        if ((S.axis == 0 ? r.oy : r.ox) != S.c) continue;
+        const double u = S.axis == 0 ? r.ox : r.oy;
+        if (!(u > S.lo && u < S.hi)) return false;
+        int b = (int)((u - S.lo) * S.scale);
+        b = b < 0 ? 0 : (b >= S.nb ? S.nb - 1 : b);
+        int e = __ldg(M.bbucket + S.boff + b);
+        double2 U = __ldg(M.bu + S.off + e);
+        while (u >= U.y && e < S.cnt - 1) U = __ldg(M.bu + S.off + (++e));
+        if (!(U.x < u && u < U.y)) return false;  // on a vertex: general path
+        const double4 PQ = ldg4d(M.bpq + S.off + e);
+        const uint32_t word = (uint32_t)__ldg(M.bword + S.off + e);
+        const int j = (int)(word & 3u);
+        const double2 P = make_double2(PQ.x, PQ.y), Q = make_double2(PQ.z, PQ.w);
+        const double2 A = __ldg(M.cxy + 3 * (int)(word >> 2) + j);  // apex corner j
+        // _contains values in the reference's form: edge i -> (corner i+1, corner i+2)
+        const double ej = sa2(P, Q, r.ox, r.oy);
+        const double e1 = sa2(Q, A, r.ox, r.oy);
+        const double e2 = sa2(A, P, r.ox, r.oy);
+        if (!(ej >= -1e-15 && e1 > 1e-12 && e2 > 1e-12)) return false;
+        const double sa = side_of(r, P), sb = side_of(r, Q);
+        if (!(sb < 0.0 && 0.0 < sa)) return false;
+        s.w = word;
+        s.sq = sa;  // side of corner (j+1)%3
+        s.sp = sb;  // side of corner (j+2)%3
+        s.fast = true;
+        s.steps = 0;  // the first walk step enters (counts) T itself
+        s.cur = (int)(word >> 2);
+        s.ei = j;
+        return true;
+    }
+    return false;
+}
+
 template <bool GEN>
 __device__ __noinline__ Init prologue(long long i, int mode, double bx0, double by0, double bx1,
                                       double by1, unsigned long long key, unsigned long long first,
-                                      const double *rays, const int32_t *start, int nt, int res,
-                                      int flood_filter, const double2 *cxy, const int4 *lnbr,
-                                      const int4 *link, const int32_t *anchor) {
-    MeshDev M{};
-    M.nt = nt;
-    M.res = res;
-    M.flood_filter = flood_filter;
-    M.cxy = cxy;
-    M.lnbr = lnbr;
-    M.link = link;
-    M.anchor = anchor;
+                                      const double *rays, const int32_t *start,
+                                      const MeshDev *__restrict__ Mg) {
+    const MeshDev &M = *Mg;
     RaySrc src{};
     src.mode = mode;
     src.box = Box{bx0, by0, bx1, by1};
@@ -482,6 +520,17 @@ __device__ __noinline__ Init prologue(long long i, int mode, double bx0, double 
     const Ray r = GEN ? gen_ray(src.mode, src.box, src.key, src.first + (unsigned long long)i)
                       : load_ray(src.rays, i);
     o.ox = r.ox; o.oy = r.oy; o.dx = r.dx; o.dy = r.dy;
+    if (!src.start) {
+        WalkState bs;
+        if (boundary_start(M, r, bs)) {
+            o.start = bs.cur;
+            o.sp = bs.sp; o.sq = bs.sq; o.w = bs.w; o.cur = bs.cur; o.ei = bs.ei; o.steps = 0;
+            o.fast = true;
+            o.phase = 1;
+            o.st = MWT_ST_BOUNDARY;
+            return o;
+        }
+    }
     double2 P0, P1, P2;
     int t0;
     if (src.start) {
@@ -515,7 +564,8 @@ __device__ __noinline__ Init prologue(long long i, int mode, double bx0, double 
 
 template <bool GEN, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
-    k_trace(MeshDev M, RaySrc src, long long n, TraceOut out, long long *hist, int refill_below) {
+    k_trace(MeshDev M, const MeshDev *__restrict__ Mg, RaySrc src, long long n, TraceOut out,
+            long long *hist, int refill_below) {
     __shared__ unsigned int h[MWT_HIST_LEN];
     if (hist) hist_init(h);
     const unsigned FULL = 0xffffffffu;
@@ -572,8 +622,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
                         idx = i;
                         const Init in = prologue<GEN>(
                             i, src.mode, src.box.x0, src.box.y0, src.box.x1, src.box.y1, src.key,
-                            src.first, src.rays, src.start, M.nt, M.res, M.flood_filter, M.cxy,
-                            M.lnbr, M.link, M.anchor);
+                            src.first, src.rays, src.start, Mg);
                         r.ox = in.ox; r.oy = in.oy; r.dx = in.dx; r.dy = in.dy;
                         s.sp = in.sp; s.sq = in.sq; s.w = in.w;
                         s.cur = in.cur; s.ei = in.ei; s.steps = in.steps;
@@ -618,7 +667,8 @@ struct LaneQ {  // SoA, one entry per lane slot
 
 template <bool GEN, int MINB>
 __global__ void __launch_bounds__(kThreads, MINB)
-    k_trace_q(MeshDev M, RaySrc src, long long n, TraceOut out, long long *hist) {
+    k_trace_q(MeshDev M, const MeshDev *__restrict__ Mg, RaySrc src, long long n, TraceOut out,
+              long long *hist) {
     __shared__ unsigned int h[MWT_HIST_LEN];
     __shared__ LaneQ qs[2 * (kThreads / 32)];
     if (hist) hist_init(h);
@@ -700,8 +750,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
                 if (i < end) {
                     const Init in = prologue<GEN>(
                         i, src.mode, src.box.x0, src.box.y0, src.box.x1, src.box.y1, src.key,
-                        src.first, src.rays, src.start, M.nt, M.res, M.flood_filter, M.cxy, M.lnbr,
-                        M.link, M.anchor);
+                        src.first, src.rays, src.start, Mg);
                     PQ.ox[lane] = in.ox; PQ.oy[lane] = in.oy; PQ.dx[lane] = in.dx; PQ.dy[lane] = in.dy;
                     PQ.sp[lane] = in.sp; PQ.sq[lane] = in.sq; PQ.idx[lane] = i; PQ.w[lane] = in.w;
                     PQ.st[lane] = in.st; PQ.cur[lane] = in.cur; PQ.ei[lane] = in.ei;
@@ -813,10 +862,10 @@ static void launch_k_trace(const MeshDev &m, const RaySrc &src, long long n, con
                            long long *hist, void *stream) {
     if (g_variant == 1) {
         k_trace<GEN, MINB><<<persistent_grid(k_trace<GEN, MINB>, n), kThreads, 0,
-                             (cudaStream_t)stream>>>(m, src, n, out, hist, g_refill_below);
+                             (cudaStream_t)stream>>>(m, m.self, src, n, out, hist, g_refill_below);
     } else {
         k_trace_q<GEN, MINB><<<persistent_grid(k_trace_q<GEN, MINB>, n), kThreads, 0,
-                               (cudaStream_t)stream>>>(m, src, n, out, hist);
+                               (cudaStream_t)stream>>>(m, m.self, src, n, out, hist);
     }
 }
 

@@ -68,6 +68,6 @@ def histogram_host(seg, steps, status=None):
     h[_lib.HIST_STEPS_SUM] = int(np.clip(steps, 0, None).sum())
     if status is not None:
         st = np.asarray(status, dtype=np.uint32)
-        for b in range(11):
+        for b in range(12):
             h[_lib.HIST_STATUS0 + b] = int(((st >> b) & 1).sum())
     return h

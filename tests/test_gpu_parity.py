@@ -12,7 +12,7 @@ from conftest import CONFIGS, box_of, fixture_paths
 pytestmark = pytest.mark.gpu
 
 T_RTOL = 1e-12
-LOC_BRUTE = np.uint32(256)
+LOC_BRUTE = np.uint32(256 | 2048)  # engine-only bits: own seed walk, boundary-table start
 
 
 def _mesh_pair(cfg, which):

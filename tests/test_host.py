@@ -108,7 +108,7 @@ def test_packer_dry_run(cfg):
     # seed grid: each cell centre inside (tolerance 1e-15) its triangle
     res = p["res"]
     cy, cx = np.mgrid[0:res, 0:res]
-    px, py = (cx + 0.5) / res, (cy + 0.5) / res
+    px, py = (cx + 0.5) * (1.0 / res), (cy + 0.5) * (1.0 / res)
     tv = tri.v[p["anchor"]]
     P = tri.vxy[tv]  # (res, res, 3, 2)
     for k in range(3):
