@@ -17,7 +17,7 @@ namespace mwt {
 //
 //   link[T]   int4  walk words, one per edge i = 0..2 (edge i is opposite
 //                   corner i, endpoints corners (i+1)%3, (i+2)%3 -- trimesh.py:10-13):
-//                     bit31 = 0  : internal edge, (nbr << 2) | mirror j
+//                     bit31 = 0  : internal edge, step-record index 3*nbr + mirror j
 //                     bit31 = 1  : walk stops here; bit30 = boundary kind,
 //                                  bits 0..29 = scene segment id (geometry hit)
 //                     0xFFFFFFFF : internal edge without neighbour (miss)

@@ -84,7 +84,7 @@ int pack_mesh(const double *vx, const double *vy, int32_t nv, const int32_t *tv,
         *err = "mesh_create: negative count or NULL array";
         return MWT_E_INVALID;
     }
-    if (nt >= (1 << 29) || ns >= (1 << 30)) {
+    if (nt >= (1 << 29) || ns >= (1 << 30)) {  // 3*nt record indices < 2^31
         *err = "mesh_create: triangulation too large for the 30-bit edge words";
         return MWT_E_INVALID;
     }
@@ -129,7 +129,7 @@ int pack_mesh(const double *vx, const double *vy, int32_t nv, const int32_t *tv,
             } else if (n < 0) {
                 w = kOpenWord;
             } else {
-                w = ((uint32_t)n << 2) | (uint32_t)j;
+                w = 3u * (uint32_t)n + (uint32_t)j;  // step record of neighbour n entered via its edge j
             }
             P.link[4LL * t + i] = (int32_t)w;
         }
@@ -207,7 +207,7 @@ int pack_mesh(const double *vx, const double *vy, int32_t nv, const int32_t *tv,
                 // tests containment with the actual coordinates
                 const double ua = axis == 0 ? vx[a] : vy[a], ub = axis == 0 ? vx[b] : vy[b];
                 es.push_back({std::min(ua, ub), std::max(ua, ub), vx[a], vy[a], vx[b], vy[b],
-                              (int32_t)(((uint32_t)t << 2) | (uint32_t)i)});
+                              (int32_t)(3 * t + i)});
             }
         if (!ok || es.empty()) continue;
         std::sort(es.begin(), es.end(), [](const E &p, const E &q) { return p.umin < q.umin; });

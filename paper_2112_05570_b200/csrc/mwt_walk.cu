@@ -201,23 +201,29 @@ __device__ __forceinline__ int locate(const MeshDev &M, double px, double py, ui
 // step loads link[N] (16 B) and the apex corner cxy[3N + j] (16 B) -- both
 // addressed by (N, j) alone.
 
+// Walk words (packer): an internal edge's word is the index k = 3N + j of the
+// step record for entering neighbour N through its edge j; stop words carry
+// the stop bit.  The walk state keeps the record index of the current
+// triangle (kr) and which candidate it exits through (ch: 0 = edge (j+1)%3,
+// 1 = edge (j+2)%3); the triangle id and exit edge are only needed at the
+// exit, and are recovered there (cur = kr / 3, ei = (kr % 3 + 1 + ch) % 3).
 struct WalkState {
-    int cur, ei, steps;
-    uint32_t w;
-    double sp, sq;  // side values of the exit edge's endpoints, corners (ei+1)%3, (ei+2)%3
+    int kr, ch, steps;
+    uint32_t w;     // word of the exit edge just chosen
+    double sp, sq;  // side values of that edge's endpoints, corners (ei+1)%3, (ei+2)%3
     bool fast;      // sp < 0 < sq: the next step may take the one-candidate fast path
 };
 
-// the 32-B step record for entering triangle w >> 2 through its edge w & 3
-__device__ __forceinline__ void load_step(const MeshDev &M, uint32_t w, int4 &W, double2 &A) {
-    const int k = 3 * (int)(w >> 2) + (int)(w & 3u);
-    W = __ldg(M.step + 2 * k);
-    A = __ldg(reinterpret_cast<const double2 *>(M.step + 2 * k + 1));
+// the 32-B step record k (words of the two candidate exits, apex corner)
+__device__ __forceinline__ void load_step(const MeshDev &M, uint32_t k, int4 &W, double2 &A) {
+    const int4 *p = M.step + 2 * (size_t)k;
+    W = __ldg(p);
+    A = __ldg(reinterpret_cast<const double2 *>(p + 1));
 }
 
 // first triangle: edges 0 (s1,s2), 1 (s2,s0), 2 (s0,s1) in order, none skipped
-__device__ __forceinline__ bool walk_first(const Ray &r, int4 L, double2 P0, double2 P1, double2 P2,
-                                           WalkState &s, uint32_t &st) {
+__device__ __forceinline__ bool walk_first(const Ray &r, int t0, int4 L, double2 P0, double2 P1,
+                                           double2 P2, WalkState &s, uint32_t &st) {
     double s0 = side_of(r, P0), s1 = side_of(r, P1), s2 = side_of(r, P2);
     int best = -1, fb = -1, ncand = 0;
     double bt = 0.0, ft = 0.0;
@@ -247,7 +253,9 @@ __device__ __forceinline__ bool walk_first(const Ray &r, int4 L, double2 P0, dou
     s.sp = best == 0 ? s1 : (best == 1 ? s2 : s0);
     s.sq = best == 0 ? s2 : (best == 1 ? s0 : s1);
     s.fast = s.sp < 0.0 && 0.0 < s.sq;
-    s.ei = best;
+    // express "exit edge best of t0" as (record, choice 0): j = (best + 2) % 3
+    s.kr = 3 * t0 + (best == 0 ? 2 : best - 1);
+    s.ch = 0;
     s.w = pick(L, best);
     return true;
 }
@@ -296,49 +304,43 @@ __device__ __forceinline__ bool walk_step(const MeshDev &M, const Ray &r, WalkSt
         return false;
     }
     s.steps++;
-    const int cur = (int)(s.w >> 2);
-    const int j = (int)(s.w & 3u);
+    const uint32_t k = s.w;
     // one 32-B step record: both candidate exit words and the apex corner
     int4 W;
     double2 A;
-    load_step(M, s.w, W, A);
-    const uint32_t w1 = (uint32_t)W.x, w2 = (uint32_t)W.y;  // edges (j+1)%3, (j+2)%3
+    load_step(M, k, W, A);
     const double c = side_of(r, A);
-    s.cur = cur;
-    int e;
+    s.kr = (int)k;
     if (s.fast && c != 0.0) {
         // (sp, sq) of the new exit: E1 -> (sp, c), E2 -> (c, sq)
         if (c > 0.0) {
             s.sq = c;
-            e = j + 1;
-            s.w = w1;
+            s.w = (uint32_t)W.x;
+            s.ch = 0;
         } else {
             s.sp = c;
-            e = j + 2;
-            s.w = w2;
+            s.w = (uint32_t)W.y;
+            s.ch = 1;
         }
-        s.ei = e >= 3 ? e - 3 : e;
         return true;
-    } else {
-        const double a = s.sq, b = s.sp;
-        const uint32_t g = walk_general(j, a, b, c, st);
-        st = g & 0xFFFFFu;
-        const int sel = (int)(g >> 20) - 1;
-        if (sel < 0) return false;
-        if (sel == 0) {  // E1
-            s.sp = b;
-            s.sq = c;
-            e = j + 1;
-            s.w = w1;
-        } else {  // E2
-            s.sp = c;
-            s.sq = a;
-            e = j + 2;
-            s.w = w2;
-        }
-        s.fast = s.sp < 0.0 && 0.0 < s.sq;
     }
-    s.ei = e >= 3 ? e - 3 : e;
+    const int j = (int)(k % 3u);
+    const double a = s.sq, b = s.sp;
+    const uint32_t g = walk_general(j, a, b, c, st);
+    st = g & 0xFFFFFu;
+    const int sel = (int)(g >> 20) - 1;
+    if (sel < 0) return false;
+    if (sel == 0) {  // E1
+        s.sp = b;
+        s.sq = c;
+        s.w = (uint32_t)W.x;
+    } else {  // E2
+        s.sp = c;
+        s.sq = a;
+        s.w = (uint32_t)W.y;
+    }
+    s.ch = sel;
+    s.fast = s.sp < 0.0 && 0.0 < s.sq;
     return true;
 }
 
@@ -357,8 +359,10 @@ __device__ __forceinline__ int walk_terminal(const MeshDev &M, const Ray &r, con
     if (!ok) {
         // grazing numerical corner, accel.py:199-207
         st |= ST_GRAZING;
-        const double2 pa = __ldg(M.cxy + 3 * s.cur + (s.ei + 1) % 3);
-        const double2 pb = __ldg(M.cxy + 3 * s.cur + (s.ei + 2) % 3);
+        const int cur = s.kr / 3, j = s.kr % 3;
+        const int ei = (j + 1 + s.ch) % 3;
+        const double2 pa = __ldg(M.cxy + 3 * cur + (ei + 1) % 3);
+        const double2 pb = __ldg(M.cxy + 3 * cur + (ei + 2) % 3);
         const double wq = s.sp != s.sq ? s.sp / (s.sp - s.sq) : 0.5;
         const double x = pa.x + wq * (pb.x - pa.x);
         const double y = pa.y + wq * (pb.y - pa.y);
@@ -382,7 +386,7 @@ struct Term {
 // state into local memory for the whole loop)
 __device__ __noinline__ Term terminal(const double4 *seg, const int2 *ep_range, const int32_t *ep_ids,
                                       const double2 *cxy, double ox, double oy, double dx, double dy,
-                                      int cur, int ei, uint32_t w, double sp, double sq, uint32_t st) {
+                                      int kr, int ch, uint32_t w, double sp, double sq, uint32_t st) {
     MeshDev M{};
     M.seg = seg;
     M.ep_range = ep_range;
@@ -390,8 +394,8 @@ __device__ __noinline__ Term terminal(const double4 *seg, const int2 *ep_range, 
     M.cxy = cxy;
     Ray r{ox, oy, dx, dy};
     WalkState s;
-    s.cur = cur;
-    s.ei = ei;
+    s.kr = kr;
+    s.ch = ch;
     s.w = w;
     s.sp = sp;
     s.sq = sq;
@@ -480,9 +484,8 @@ __device__ __forceinline__ bool boundary_start(const MeshDev &M, const Ray &r, W
         if (!(U.x < u && u < U.y)) return false;  // on a vertex: general path
         const double4 PQ = ldg4d(M.bpq + S.off + e);
         const uint32_t word = (uint32_t)__ldg(M.bword + S.off + e);
-        const int j = (int)(word & 3u);
         const double2 P = make_double2(PQ.x, PQ.y), Q = make_double2(PQ.z, PQ.w);
-        const double2 A = __ldg(M.cxy + 3 * (int)(word >> 2) + j);  // apex corner j
+        const double2 A = __ldg(M.cxy + word);  // apex corner j of T: cxy[3T + j], word = 3T + j
         // _contains values in the reference's form: edge i -> (corner i+1, corner i+2)
         const double ej = sa2(P, Q, r.ox, r.oy);
         const double e1 = sa2(Q, A, r.ox, r.oy);
@@ -495,8 +498,8 @@ __device__ __forceinline__ bool boundary_start(const MeshDev &M, const Ray &r, W
         s.sp = sb;  // side of corner (j+2)%3
         s.fast = true;
         s.steps = 0;  // the first walk step enters (counts) T itself
-        s.cur = (int)(word >> 2);
-        s.ei = j;
+        s.kr = (int)word;
+        s.ch = 0;
         return true;
     }
     return false;
@@ -523,8 +526,8 @@ __device__ __noinline__ Init prologue(long long i, int mode, double bx0, double 
     if (!src.start) {
         WalkState bs;
         if (boundary_start(M, r, bs)) {
-            o.start = bs.cur;
-            o.sp = bs.sp; o.sq = bs.sq; o.w = bs.w; o.cur = bs.cur; o.ei = bs.ei; o.steps = 0;
+            o.start = bs.kr / 3;
+            o.sp = bs.sp; o.sq = bs.sq; o.w = bs.w; o.cur = bs.kr; o.ei = bs.ch; o.steps = 0;
             o.fast = true;
             o.phase = 1;
             o.st = MWT_ST_BOUNDARY;
@@ -542,22 +545,22 @@ __device__ __noinline__ Init prologue(long long i, int mode, double bx0, double 
     }
     o.start = t0;
     WalkState s;
-    s.cur = t0;
+    s.kr = 0;
+    s.ch = 0;
     s.steps = 1;
     s.sp = s.sq = 0.0;
-    s.ei = 0;
     s.w = 0;
     s.fast = false;
     if (t0 < 0) {
         o.st |= ST_ERROR;
         s.steps = 0;
         o.phase = 3;
-    } else if (!walk_first(r, __ldg(M.link + t0), P0, P1, P2, s, o.st)) {
+    } else if (!walk_first(r, t0, __ldg(M.link + t0), P0, P1, P2, s, o.st)) {
         o.phase = 3;
     } else {
         o.phase = (s.w & kStopBit) ? 2 : 1;
     }
-    o.sp = s.sp; o.sq = s.sq; o.w = s.w; o.cur = s.cur; o.ei = s.ei; o.steps = s.steps;
+    o.sp = s.sp; o.sq = s.sq; o.w = s.w; o.cur = s.kr; o.ei = s.ch; o.steps = s.steps;
     o.fast = s.fast;
     return o;
 }
@@ -596,7 +599,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
                 double t = CUDART_NAN, u = CUDART_NAN;
                 if (phase == 2) {
                     const Term tm = terminal(M.seg, M.ep_range, M.ep_ids, M.cxy, r.ox, r.oy, r.dx,
-                                             r.dy, s.cur, s.ei, s.w, s.sp, s.sq, st);
+                                             r.dy, s.kr, s.ch, s.w, s.sp, s.sq, st);
                     seg = tm.seg;
                     t = tm.t;
                     u = tm.u;
@@ -625,7 +628,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
                             src.first, src.rays, src.start, Mg);
                         r.ox = in.ox; r.oy = in.oy; r.dx = in.dx; r.dy = in.dy;
                         s.sp = in.sp; s.sq = in.sq; s.w = in.w;
-                        s.cur = in.cur; s.ei = in.ei; s.steps = in.steps;
+                        s.kr = in.cur; s.ch = in.ei; s.steps = in.steps;
                         s.fast = in.fast;
                         st = in.st;
                         phase = in.phase;
@@ -640,9 +643,13 @@ __global__ void __launch_bounds__(kThreads, MINB)
                 continue;  // pending lanes resolve at the top of the loop
             }
         }
-        if (phase == 1) {
-            if (!walk_step(M, r, s, st)) phase = 3;
-            else if (s.w & kStopBit) phase = 2;
+        // several steps per refill check: amortises the ballot / refill bookkeeping
+#pragma unroll
+        for (int u2 = 0; u2 < 2; u2++) {
+            if (phase == 1) {
+                if (!walk_step(M, r, s, st)) phase = 3;
+                else if (s.w & kStopBit) phase = 2;
+            }
         }
     }
     if (hist) hist_flush(h, steps_sum, hist);
@@ -735,7 +742,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
                 const int k = epi_n + __popc(pend & lt_mask);
                 EQ.ox[k] = r.ox; EQ.oy[k] = r.oy; EQ.dx[k] = r.dx; EQ.dy[k] = r.dy;
                 EQ.sp[k] = s.sp; EQ.sq[k] = s.sq; EQ.idx[k] = idx; EQ.w[k] = s.w; EQ.st[k] = st;
-                EQ.cur[k] = s.cur; EQ.ei[k] = s.ei; EQ.steps[k] = s.steps;
+                EQ.cur[k] = s.kr; EQ.ei[k] = s.ch; EQ.steps[k] = s.steps;
                 EQ.phase[k] = (unsigned char)phase;
                 phase = 0;
             }
@@ -770,7 +777,7 @@ __global__ void __launch_bounds__(kThreads, MINB)
                     const int k = pro_h + rank;
                     r.ox = PQ.ox[k]; r.oy = PQ.oy[k]; r.dx = PQ.dx[k]; r.dy = PQ.dy[k];
                     s.sp = PQ.sp[k]; s.sq = PQ.sq[k]; idx = PQ.idx[k]; s.w = PQ.w[k]; st = PQ.st[k];
-                    s.cur = PQ.cur[k]; s.ei = PQ.ei[k]; s.steps = PQ.steps[k];
+                    s.kr = PQ.cur[k]; s.ch = PQ.ei[k]; s.steps = PQ.steps[k];
                     s.fast = PQ.fast[k] != 0;
                     phase = PQ.phase[k];
                 }

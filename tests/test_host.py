@@ -92,7 +92,9 @@ def test_packer_dry_run(cfg):
     stop = (link & 0x80000000) != 0
     assert np.array_equal(stop, (tri.flag != -1) | (tri.nbr == -1))
     internal = ~stop
-    assert np.array_equal((link[internal] >> 2).astype(np.int32), tri.nbr[internal])
+    # internal word = step-record index 3 * nbr + mirror
+    assert np.array_equal((link[internal] // 3).astype(np.int32), tri.nbr[internal])
+    assert np.array_equal((link[internal] % 3).astype(np.int32), p["lnbr"][:, :3][internal] & 3)
     assert np.array_equal(lnbr >= 0, tri.nbr >= 0)
     has = lnbr >= 0
     assert np.array_equal(lnbr[has] >> 2, tri.nbr[has])

@@ -45,10 +45,10 @@ norm = re.sub(r"\(bool\)1", "true", re.sub(r"\(bool\)0", "false", kname))
 norm = re.sub(r"\(int\)(-?\d+)", r"\1", norm).replace(" ", "")
 for f in cand:
     dem = subprocess.run(["c++filt", f], capture_output=True, text=True).stdout.strip().replace(" ", "")
-    if dem == norm:
+    if dem.split("(")[0] == norm.split("(")[0]:
         want = f
 if want is None:
-    want = cand[0]
+    raise SystemExit(f"no SASS function matches {kname!r}")
 body = text.split(f".text.{want}:\n", 1)[1].split("//---------------------", 1)[0]
 linemap = {}
 cur = None
