@@ -149,7 +149,7 @@ static inline double u01(uint64_t s0, uint64_t k) {
 
 /* mode 0: box-entry isotropic line rays; mode 1: interior origins */
 void orc_raygen_one(int mode, const double box[4], uint64_t key, uint64_t idx, double out[4]) {
-    uint64_t s0 = mix64(key ^ idx);
+    uint64_t s0 = key ^ idx; /* per-ray SplitMix64 stream: mix64(s0 + (k + 1) * golden) */
     double x = 1.0, y = 0.0, r2 = 1.0;
     int ok = 0;
     for (int a = 0; a < 64; a++) {

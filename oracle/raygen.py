@@ -54,7 +54,7 @@ def raygen(mode: int, box, seed: int, first: int, n: int) -> np.ndarray:
     """(n, 4) float64 array of rays (ox, oy, dx, dy)."""
     key = ray_key(seed, mode)
     idx = np.arange(first, first + n, dtype=np.uint64)
-    s0 = _mix(key ^ idx)
+    s0 = key ^ idx  # per-ray SplitMix64 stream: draws mix64(s0 + (k + 1) * golden)
     x = np.ones(n)
     y = np.zeros(n)
     r2 = np.ones(n)

@@ -179,7 +179,8 @@ struct Box {
 
 __device__ __forceinline__ Ray gen_ray(int mode, const Box &b, unsigned long long key,
                                        unsigned long long idx) {
-    unsigned long long s0 = mix64(key ^ idx);
+    // per-ray SplitMix64 stream: draws mix64(s0 + (k + 1) * golden), s0 = key ^ index
+    const unsigned long long s0 = key ^ idx;
     // unit-disk rejection: the first accepted attempt a in 0..63.  Attempts 0
     // and 1 are evaluated unconditionally (accepted together with probability
     // 1 - (1 - pi/4)^2 = 95%) so the warp stays converged; the rest is a rare loop.

@@ -62,6 +62,7 @@ struct HostPacked {
     std::vector<int32_t> anchor;    // res*res
     // boundary-edge table (box-entry start triangles), one side per boundary segment
     int32_t nbsides = 0;
+    int32_t unit_sides = 0;  // sides are exactly y=0, x=1, y=1, x=0 (in this order)
     struct Side {
         int32_t axis;      // 0: side lies on y = c (u = x); 1: on x = c (u = y)
         double c, lo, hi;  // the line, and the side's u extent
@@ -96,6 +97,7 @@ struct MeshDev {
     double inv_res;  // 1.0 / res (seed-cell centres: (c + 0.5) * inv_res)
     // boundary-edge table: start triangles of rays whose origin lies on a box side
     int32_t nbsides;
+    int32_t unit_sides;  // sides ordered y=0, x=1, y=1, x=0: the side is found without loads
     struct BSide {
         int32_t axis, off, cnt, boff, nb;
         double c, lo, hi, scale;

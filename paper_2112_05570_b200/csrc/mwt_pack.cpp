@@ -241,6 +241,27 @@ int pack_mesh(const double *vx, const double *vy, int32_t nv, const int32_t *tv,
             P.bbucket.push_back(k);
         }
     }
+    // the unit square (every mintri scene, scene.py:18-23): order the sides
+    // bottom, right, top, left so the device picks the side from the origin
+    P.unit_sides = 0;
+    if (P.nbsides == 4) {
+        int order[4] = {-1, -1, -1, -1};
+        for (int k = 0; k < 4; k++) {
+            const HostPacked::Side &S = P.sides[k];
+            int slot = -1;
+            if (S.axis == 0 && S.c == 0.0) slot = 0;
+            else if (S.axis == 1 && S.c == 1.0) slot = 1;
+            else if (S.axis == 0 && S.c == 1.0) slot = 2;
+            else if (S.axis == 1 && S.c == 0.0) slot = 3;
+            if (slot >= 0 && order[slot] < 0) order[slot] = k;
+        }
+        if (order[0] >= 0 && order[1] >= 0 && order[2] >= 0 && order[3] >= 0) {
+            HostPacked::Side tmp[4];
+            for (int k = 0; k < 4; k++) tmp[k] = P.sides[order[k]];
+            for (int k = 0; k < 4; k++) P.sides[k] = tmp[k];
+            P.unit_sides = 1;
+        }
+    }
     if (P.bword.empty()) {  // keep device pointers valid
         P.bu.assign(2, 0.0);
         P.bpq.assign(4, 0.0);

@@ -471,7 +471,13 @@ struct Init {
 // and has trans < 0, so neither the exit nor the fallback choice can pick it.
 __device__ __forceinline__ bool boundary_start(const MeshDev &M, const Ray &r, WalkState &s) {
     if (!(M.flood_filter && fabs(r.ox) <= 4.0 && fabs(r.oy) <= 4.0)) return false;
-    for (int k = 0; k < M.nbsides; k++) {
+    int k0 = 0, k1 = M.nbsides;
+    if (M.unit_sides) {  // bottom, right, top, left
+        k0 = r.oy == 0.0 ? 0 : (r.ox == 1.0 ? 1 : (r.oy == 1.0 ? 2 : (r.ox == 0.0 ? 3 : -1)));
+        if (k0 < 0) return false;
+        k1 = k0 + 1;
+    }
+    for (int k = k0; k < k1; k++) {
         const MeshDev::BSide &S = M.bs[k];
         if ((S.axis == 0 ? r.oy : r.ox) != S.c) continue;
         const double u = S.axis == 0 ? r.ox : r.oy;

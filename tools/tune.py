@@ -21,7 +21,7 @@ if not os.path.exists(os.path.join(d, f"{which}.tri")):
 mesh = DeviceMesh.from_files(os.path.join(d, "scene.txt"), os.path.join(d, f"{which}.tri"))
 hist = new_histogram()
 res = []
-combos = [(0, m, 0) for m in (2, 3, 4)] + [(r, m, 1) for m in (2, 3) for r in (4, 8)]
+combos = [(0, 2, 0)] + [(r, m, 1) for m in (2, 3, 4) for r in (2, 4, 8)]
 for refill, minb, variant in combos:
     if True:
         _lib.lib.mwt_set_tuning(refill, minb, variant)
