@@ -59,8 +59,12 @@ T *carve(Arena &a, size_t count) {
 
 }  // namespace
 
+constexpr int kHostStreams = 3;
+constexpr int64_t kHostChunk = 1 << 20;  // rays per pipelined chunk of mwt_trace_host
+
 struct mwt_mesh {
     int device = 0;
+    cudaStream_t hstream[kHostStreams] = {nullptr, nullptr, nullptr};
     mwt::MeshDev dev{};
     mwt_mesh_info info{};
     void *blob = nullptr;
@@ -219,6 +223,8 @@ int mwt_mesh_destroy(mwt_mesh *m) {
     if (!m) return MWT_OK;
     DeviceGuard g(m->device);
     if (m->stream) cudaStreamDestroy(m->stream);
+    for (int k = 0; k < kHostStreams; k++)
+        if (m->hstream[k]) cudaStreamDestroy(m->hstream[k]);
     if (m->scratch) cudaFree(m->scratch);
     if (m->blob) cudaFree(m->blob);
     delete m;
@@ -280,9 +286,16 @@ int mwt_trace_host(const mwt_mesh *cm, const double *rays, const int32_t *start,
     if (n == 0) return MWT_OK;
     std::lock_guard<std::mutex> lk(m->mu);
     DeviceGuard g(m->device);
-    // per-ray device bytes: rays 32 + start 4 + outputs 4+4+8+8+4+4
-    const size_t per = 32 + 4 + 4 + 4 + 8 + 8 + 4 + 4;
-    size_t need = (size_t)n * per + 8 * 256;
+    // Chunked pipeline over kHostStreams streams: chunk k's H2D copy, trace and
+    // D2H copies are ordered on stream k % kHostStreams, so host->device and
+    // device->host copies of different chunks overlap each other (separate copy
+    // engines) and the kernels.  With pinned host buffers the call is bounded by
+    // the larger copy direction.
+    const int64_t chunk = n < kHostChunk ? n : kHostChunk;
+    const size_t per = 32 + 4 + 4 + 4 + 8 + 8 + 4 + 4;  // rays, start, 6 outputs
+    const size_t slot = Arena::align((size_t)chunk * 32) + 7 * Arena::align((size_t)chunk * 8);
+    const size_t need = kHostStreams * slot;
+    (void)per;
     if (need > m->scratch_bytes) {
         if (m->scratch) cudaFree(m->scratch);
         m->scratch = nullptr;
@@ -290,32 +303,39 @@ int mwt_trace_host(const mwt_mesh *cm, const double *rays, const int32_t *start,
         CK(cudaMalloc(&m->scratch, need));
         m->scratch_bytes = need;
     }
-    Arena a;
-    a.base = (char *)m->scratch;
-    a.size = need;
-    double *d_rays = carve<double>(a, 4 * n);
-    int32_t *d_start = carve<int32_t>(a, n);
-    int32_t *d_ostart = carve<int32_t>(a, n);
-    int32_t *d_seg = carve<int32_t>(a, n);
-    double *d_t = carve<double>(a, n);
-    double *d_u = carve<double>(a, n);
-    int32_t *d_steps = carve<int32_t>(a, n);
-    uint32_t *d_st = carve<uint32_t>(a, n);
-    cudaStream_t s = m->stream;
-    CK(cudaMemcpyAsync(d_rays, rays, 32 * (size_t)n, cudaMemcpyHostToDevice, s));
-    if (start) CK(cudaMemcpyAsync(d_start, start, 4 * (size_t)n, cudaMemcpyHostToDevice, s));
-    int rc = mwt::launch_trace(m->dev, d_rays, start ? d_start : nullptr, n,
-                               out_start ? d_ostart : nullptr, out_seg ? d_seg : nullptr,
-                               out_t ? d_t : nullptr, out_u ? d_u : nullptr,
-                               out_steps ? d_steps : nullptr, out_status ? d_st : nullptr, s);
-    if (rc) return cuda_fail((cudaError_t)rc, "trace_host launch");
-    if (out_start) CK(cudaMemcpyAsync(out_start, d_ostart, 4 * (size_t)n, cudaMemcpyDeviceToHost, s));
-    if (out_seg) CK(cudaMemcpyAsync(out_seg, d_seg, 4 * (size_t)n, cudaMemcpyDeviceToHost, s));
-    if (out_t) CK(cudaMemcpyAsync(out_t, d_t, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));
-    if (out_u) CK(cudaMemcpyAsync(out_u, d_u, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));
-    if (out_steps) CK(cudaMemcpyAsync(out_steps, d_steps, 4 * (size_t)n, cudaMemcpyDeviceToHost, s));
-    if (out_status) CK(cudaMemcpyAsync(out_status, d_st, 4 * (size_t)n, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
+    for (int k = 0; k < kHostStreams; k++)
+        if (!m->hstream[k]) CK(cudaStreamCreateWithFlags(&m->hstream[k], cudaStreamNonBlocking));
+    const int64_t nchunks = (n + chunk - 1) / chunk;
+    for (int64_t c = 0; c < nchunks; c++) {
+        const int k = (int)(c % kHostStreams);
+        const int64_t off = c * chunk, cnt = (n - off) < chunk ? (n - off) : chunk;
+        Arena a;
+        a.base = (char *)m->scratch + k * slot;
+        a.size = slot;
+        double *d_rays = carve<double>(a, 4 * (size_t)chunk);
+        int32_t *d_start = carve<int32_t>(a, chunk);
+        int32_t *d_ostart = carve<int32_t>(a, chunk);
+        int32_t *d_seg = carve<int32_t>(a, chunk);
+        double *d_t = carve<double>(a, chunk);
+        double *d_u = carve<double>(a, chunk);
+        int32_t *d_steps = carve<int32_t>(a, chunk);
+        uint32_t *d_st = carve<uint32_t>(a, chunk);
+        cudaStream_t s = m->hstream[k];
+        CK(cudaMemcpyAsync(d_rays, rays + 4 * off, 32 * (size_t)cnt, cudaMemcpyHostToDevice, s));
+        if (start) CK(cudaMemcpyAsync(d_start, start + off, 4 * (size_t)cnt, cudaMemcpyHostToDevice, s));
+        int rc = mwt::launch_trace(m->dev, d_rays, start ? d_start : nullptr, cnt,
+                                   out_start ? d_ostart : nullptr, out_seg ? d_seg : nullptr,
+                                   out_t ? d_t : nullptr, out_u ? d_u : nullptr,
+                                   out_steps ? d_steps : nullptr, out_status ? d_st : nullptr, s);
+        if (rc) return cuda_fail((cudaError_t)rc, "trace_host launch");
+        if (out_start) CK(cudaMemcpyAsync(out_start + off, d_ostart, 4 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
+        if (out_seg) CK(cudaMemcpyAsync(out_seg + off, d_seg, 4 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
+        if (out_t) CK(cudaMemcpyAsync(out_t + off, d_t, 8 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
+        if (out_u) CK(cudaMemcpyAsync(out_u + off, d_u, 8 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
+        if (out_steps) CK(cudaMemcpyAsync(out_steps + off, d_steps, 4 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
+        if (out_status) CK(cudaMemcpyAsync(out_status + off, d_st, 4 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
+    }
+    for (int k = 0; k < kHostStreams; k++) CK(cudaStreamSynchronize(m->hstream[k]));
     return MWT_OK;
 }
 

@@ -859,15 +859,30 @@ static int g_variant = 1;      // 1: refill kernel (k_trace, measured faster); 0
 
 template <typename K>
 static int persistent_grid(K kernel, long long n) {
-    int dev = 0, sms = 0, blocks_per_sm = 0;
+    // one resident wave: SMs x resident CTAs (cached per kernel and device)
+    static const void *keys[32];
+    static int devs[32], waves[32], nkeys = 0;
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kernel, kThreads, 0);
-    if (blocks_per_sm <= 0) blocks_per_sm = 1;
-    if (sms <= 0) sms = 148;
+    int wave = 0;
+    for (int k = 0; k < nkeys; k++)
+        if (keys[k] == (const void *)kernel && devs[k] == dev) wave = waves[k];
+    if (wave == 0) {
+        int sms = 0, blocks_per_sm = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kernel, kThreads, 0);
+        if (blocks_per_sm <= 0) blocks_per_sm = 1;
+        if (sms <= 0) sms = 148;
+        wave = sms * blocks_per_sm;
+        if (nkeys < 32) {
+            keys[nkeys] = (const void *)kernel;
+            devs[nkeys] = dev;
+            waves[nkeys] = wave;
+            nkeys++;
+        }
+    }
     long long want = (n + kThreads - 1) / kThreads;
-    long long cap = (long long)sms * blocks_per_sm;  // one resident wave
-    return (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+    return (int)(want < wave ? (want < 1 ? 1 : want) : wave);
 }
 
 template <bool GEN, int MINB>
