@@ -13,6 +13,7 @@ Usage: python tests/golden/make_golden.py [group ...]
 """
 from __future__ import annotations
 
+import json
 import math
 import os
 import random
@@ -280,6 +281,23 @@ def make_struct(cfg, nrays=1024):
     np.savez_compressed(os.path.join(HERE, f"struct_{cfg}.npz"), **out)
 
 
+def make_experiment():
+    """Reference sample_rays + run_experiment on Lines-1024 (both meshes, all
+    7 c_t), for the device run_experiment (report JSON without timings)."""
+    from mintri.experiment import run_experiment
+    d = os.path.join(FIX, "lines1024")
+    scene = Scene.load(os.path.join(d, "scene.txt"))
+    tris = [load_triangulation(os.path.join(d, f"{w}.tri"), scene) for w in ("cdt", "mwt")]
+    rays = sample_rays(scene, 3000, seed=11)
+    rep = run_experiment(scene, tris, rays, labels=["cdt", "mwt"])
+    payload = json.loads(rep.to_json())
+    payload.pop("timing")
+    small = sample_rays(scene, 5000, seed=5)
+    np.savez_compressed(os.path.join(HERE, "experiment.npz"),
+                        rays=ray_arr(rays), report=np.array(json.dumps(payload, sort_keys=True)),
+                        csv=np.array(rep.to_csv()), sample5000_seed5=ray_arr(small))
+
+
 if __name__ == "__main__":
     groups = sys.argv[1:] or ["known", "hypot"] + [f"config:{c}" for c in CONFIGS] + \
         [f"struct:{c}" for c in CONFIGS[1:]]
@@ -288,6 +306,8 @@ if __name__ == "__main__":
             make_known()
         elif g == "hypot":
             make_hypot()
+        elif g == "experiment":
+            make_experiment()
         elif g.startswith("config:"):
             make_config(g.split(":", 1)[1])
         elif g.startswith("struct:"):
