@@ -161,36 +161,27 @@ void orc_raygen_one(int mode, const double box[4], uint64_t key, uint64_t idx, d
         if (r2 <= 1.0 && r2 > 0x1p-60) { ok = 1; break; }
     }
     double dx = 1.0, dy = 0.0;
-    if (ok) {
-        double inv = 1.0 / sqrt(r2);
-        dx = x * inv;
-        dy = y * inv;
+    if (ok) { /* angle doubling: (x^2 - y^2, 2xy) / r2 */
+        double inv = 1.0 / r2;
+        dx = (x * x - y * y) * inv;
+        dy = (2.0 * x * y) * inv;
     }
     double x0 = box[0], y0 = box[1], x1 = box[2], y1 = box[3];
     double W = x1 - x0, H = y1 - y0;
+    double u = u01(s0, 128), v = u01(s0, 129);
     double ox, oy;
     if (mode == 1) {
-        ox = x0 + W * u01(s0, 128);
-        oy = y0 + H * u01(s0, 129);
+        ox = x0 + W * u;
+        oy = y0 + H * v;
     } else {
-        double cx = x0 + 0.5 * W, cy = y0 + 0.5 * H;
-        double nx = -dy, ny = dx;
-        double w = 0.5 * (fabs(nx) * W + fabs(ny) * H);
-        double s = w * (2.0 * u01(s0, 128) - 1.0);
-        double px = cx + s * nx, py = cy + s * ny;
-        double tx = -INFINITY, ty = -INFINITY;
-        if (dx > 0.0) tx = (x0 - px) / dx;
-        else if (dx < 0.0) tx = (x1 - px) / dx;
-        if (dy > 0.0) ty = (y0 - py) / dy;
-        else if (dy < 0.0) ty = (y1 - py) / dy;
-        if (tx >= ty) {
+        /* entry side by projected length, uniform position along it */
+        double wx = H * fabs(dx), wy = W * fabs(dy);
+        if (u * (wx + wy) < wx) {
             ox = dx > 0.0 ? x0 : x1;
-            oy = py + tx * dy;
-            oy = oy < y0 ? y0 : (oy > y1 ? y1 : oy);
+            oy = y0 + H * v;
         } else {
             oy = dy > 0.0 ? y0 : y1;
-            ox = px + ty * dx;
-            ox = ox < x0 ? x0 : (ox > x1 ? x1 : ox);
+            ox = x0 + W * v;
         }
     }
     out[0] = ox; out[1] = oy; out[2] = dx; out[3] = dy;

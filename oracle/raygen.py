@@ -45,11 +45,6 @@ def _u01(s0, k: int):
     return (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
 
 
-def _clamp(v, lo, hi):
-    # C's ``v < lo ? lo : (v > hi ? hi : v)`` (keeps the sign of a zero)
-    return np.where(v < lo, lo, np.where(v > hi, hi, v))
-
-
 def raygen(mode: int, box, seed: int, first: int, n: int) -> np.ndarray:
     """(n, 4) float64 array of rays (ox, oy, dx, dy)."""
     key = ray_key(seed, mode)
@@ -75,27 +70,22 @@ def raygen(mode: int, box, seed: int, first: int, n: int) -> np.ndarray:
         y[sel] = ya
         r2[sel] = ra
         ok[sel[acc]] = True
-    inv = 1.0 / np.sqrt(r2)
-    dx = np.where(ok, x * inv, 1.0)
-    dy = np.where(ok, y * inv, 0.0)
+    # angle doubling: (x^2 - y^2, 2xy) / r2 is isotropic and unit up to rounding
+    inv = 1.0 / r2
+    dx = np.where(ok, (x * x - y * y) * inv, 1.0)
+    dy = np.where(ok, (2.0 * x * y) * inv, 0.0)
     x0, y0, x1, y1 = (float(v) for v in box)
     W, H = x1 - x0, y1 - y0
+    u, v = _u01(s0, 128), _u01(s0, 129)
     if mode == MODE_INTERIOR:
-        ox = x0 + W * _u01(s0, 128)
-        oy = y0 + H * _u01(s0, 129)
+        ox = x0 + W * u
+        oy = y0 + H * v
     else:
-        cx, cy = x0 + 0.5 * W, y0 + 0.5 * H
-        nx, ny = -dy, dx
-        w = 0.5 * (np.abs(nx) * W + np.abs(ny) * H)
-        s = w * (2.0 * _u01(s0, 128) - 1.0)
-        px, py = cx + s * nx, cy + s * ny
-        with np.errstate(divide="ignore", invalid="ignore"):
-            tx = np.where(dx > 0.0, (x0 - px) / dx, np.where(dx < 0.0, (x1 - px) / dx, -np.inf))
-            ty = np.where(dy > 0.0, (y0 - py) / dy, np.where(dy < 0.0, (y1 - py) / dy, -np.inf))
-        xside = tx >= ty
-        with np.errstate(invalid="ignore"):
-            oy_x = _clamp(py + tx * dy, y0, y1)
-            ox_y = _clamp(px + ty * dx, x0, x1)
-        ox = np.where(xside, np.where(dx > 0.0, x0, x1), ox_y)
-        oy = np.where(xside, oy_x, np.where(dy > 0.0, y0, y1))
+        # entry side with probability proportional to its projected length,
+        # uniform position along it (isotropic lines through the box)
+        wx = H * np.abs(dx)
+        wy = W * np.abs(dy)
+        xside = u * (wx + wy) < wx
+        ox = np.where(xside, np.where(dx > 0.0, x0, x1), x0 + W * v)
+        oy = np.where(xside, y0 + H * v, np.where(dy > 0.0, y0, y1))
     return np.ascontiguousarray(np.stack([ox, oy, dx, dy], axis=1))

@@ -201,34 +201,29 @@ __device__ __forceinline__ Ray gen_ray(int mode, const Box &b, unsigned long lon
     }
     Ray r;
     {
-        const double inv = 1.0 / sqrt(ok ? r2 : 1.0);
-        r.dx = ok ? x * inv : 1.0;
-        r.dy = ok ? y * inv : 0.0;
+        // angle doubling: (x, y) = rho (cos phi, sin phi) uniform in the disk has
+        // phi ~ U[0, 2pi), so (x^2 - y^2, 2xy) / r2 = (cos 2phi, sin 2phi) is
+        // isotropic and unit up to rounding -- no sqrt, one division
+        const double inv = 1.0 / (ok ? r2 : 1.0);
+        r.dx = ok ? (x * x - y * y) * inv : 1.0;
+        r.dy = ok ? (2.0 * x * y) * inv : 0.0;
     }
-    double W = b.x1 - b.x0, H = b.y1 - b.y0;
+    const double W = b.x1 - b.x0, H = b.y1 - b.y0;
+    const double u = u01(s0, 128), v = u01(s0, 129);
     if (mode == MWT_RAYS_INTERIOR) {
-        r.ox = b.x0 + W * u01(s0, 128);
-        r.oy = b.y0 + H * u01(s0, 129);
+        r.ox = b.x0 + W * u;
+        r.oy = b.y0 + H * v;
     } else {
-        double cx = b.x0 + 0.5 * W, cy = b.y0 + 0.5 * H;
-        double nx = -r.dy, ny = r.dx;
-        double w = 0.5 * (fabs(nx) * W + fabs(ny) * H);
-        double s = w * (2.0 * u01(s0, 128) - 1.0);
-        double px = cx + s * nx, py = cy + s * ny;
-        // entry parameter per slab: (x0 - px)/dx if dx > 0, (x1 - px)/dx if dx < 0,
-        // -inf if dx == 0 (one division per axis, no divergence)
-        const double qx = (r.dx > 0.0 ? b.x0 : b.x1) - px;
-        const double qy = (r.dy > 0.0 ? b.y0 : b.y1) - py;
-        const double tx = r.dx != 0.0 ? qx / r.dx : -CUDART_INF;
-        const double ty = r.dy != 0.0 ? qy / r.dy : -CUDART_INF;
-        if (tx >= ty) {
+        // lines of direction d with a uniform perpendicular offset enter the box
+        // through the side facing -d in x with probability H|dx| / (H|dx| + W|dy|),
+        // else through the side facing -d in y, uniformly along that side
+        const double wx = H * fabs(r.dx), wy = W * fabs(r.dy);
+        if (u * (wx + wy) < wx) {
             r.ox = r.dx > 0.0 ? b.x0 : b.x1;
-            double oy = py + tx * r.dy;
-            r.oy = oy < b.y0 ? b.y0 : (oy > b.y1 ? b.y1 : oy);
+            r.oy = b.y0 + H * v;
         } else {
             r.oy = r.dy > 0.0 ? b.y0 : b.y1;
-            double ox = px + ty * r.dx;
-            r.ox = ox < b.x0 ? b.x0 : (ox > b.x1 ? b.x1 : ox);
+            r.ox = b.x0 + W * v;
         }
     }
     return r;
