@@ -11,7 +11,7 @@ import os
 
 from . import build as _build
 
-LIB_PATH = _build.LIB
+LIB_PATH = os.environ.get("MWT_LIB_PATH", _build.LIB)  # override: A/B of builds
 
 # include/mwt.h constants
 ST_ERROR = 1
