@@ -86,11 +86,12 @@ int mwt_abi_version(void);
 const char *mwt_last_error(void);
 int mwt_device_count(int *count);
 /* Tuning knobs of the persistent walk kernel (process-wide; -1 = keep).
- * `variant` 1 = refill batches (default): idle lanes refill once at most
- * `refill_below` (default 4) lanes still walk; 0 = per-warp shared-memory
- * queues with bulk prologue/epilogue.  `min_blocks_per_sm` in {2,3,4}
- * selects the register budget of the compiled kernel (256-thread CTAs;
- * default 3 = 80 registers). */
+ * Lanes whose rays ended refill in one batch once at most `refill_below`
+ * (default 4) lanes of the warp still walk.  `variant` 2 (default) stages the
+ * mesh's compact walk table in shared memory (1024-thread CTAs, one per SM)
+ * when it fits, else runs variant 1: walk records read from global memory,
+ * 256-thread CTAs, `min_blocks_per_sm` in {2,3,4} selecting the register
+ * budget (default 4 = 64 registers). */
 int mwt_set_tuning(int refill_below, int min_blocks_per_sm, int variant);
 
 /* K1 -- mesh packer.

@@ -124,7 +124,8 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
                    Arena::align(P.ep_ids.size() * 4) + Arena::align(P.anchor.size() * 4) +
                    Arena::align(P.bu.size() * 8) + Arena::align(P.bpq.size() * 8) +
                    Arena::align(P.bword.size() * 4) + Arena::align(P.bbucket.size() * 4) +
-                   Arena::align(sizeof(mwt::MeshDev));
+                   Arena::align(sizeof(mwt::MeshDev)) + Arena::align(P.crec.size() * 4) +
+                   Arena::align(P.vxy.size() * 8);
     Arena a;
     CK(cudaMalloc(&a.base, bytes));
     a.size = bytes;
@@ -145,6 +146,8 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     int32_t *bword = carve<int32_t>(a, P.bword.size());
     int32_t *bbucket = carve<int32_t>(a, P.bbucket.size());
     mwt::MeshDev *self = carve<mwt::MeshDev>(a, 1);
+    uint32_t *crec = carve<uint32_t>(a, P.crec.size());
+    double *vxy = carve<double>(a, P.vxy.size());
     cudaError_t e = cudaSuccess;
     auto up = [&](void *dst, const void *src, size_t n) {
         if (e == cudaSuccess && n) e = cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
@@ -162,6 +165,8 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     up(bpq, P.bpq.data(), P.bpq.size() * 8);
     up(bword, P.bword.data(), P.bword.size() * 4);
     up(bbucket, P.bbucket.data(), P.bbucket.size() * 4);
+    up(crec, P.crec.data(), P.crec.size() * 4);
+    up(vxy, P.vxy.data(), P.vxy.size() * 8);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         cudaFree(a.base);
@@ -180,6 +185,13 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     m->dev.bpq = reinterpret_cast<const double4 *>(bpq);
     m->dev.bword = bword;
     m->dev.bbucket = bbucket;
+    if (!P.crec.empty()) {
+        m->dev.crec = reinterpret_cast<const uint2 *>(crec);
+        m->dev.vxy = reinterpret_cast<const double2 *>(vxy);
+        m->dev.crec_bytes = (int32_t)(P.crec.size() * 4);
+        const int64_t sm = (int64_t)m->dev.crec_bytes + 16LL * P.nv;
+        m->dev.smem_bytes = sm <= mwt::kSmemWalkMax ? (int32_t)sm : 0;
+    }
     m->dev.self = self;
     {
         cudaError_t e2 = cudaMemcpy(self, &m->dev, sizeof(mwt::MeshDev), cudaMemcpyHostToDevice);

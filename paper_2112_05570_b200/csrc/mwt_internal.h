@@ -74,7 +74,27 @@ struct HostPacked {
     std::vector<double> bpq;        // 4 per edge: P (corner (j+1)%3), Q (corner (j+2)%3)
     std::vector<int32_t> bword;     // (T << 2) | j, j = the boundary edge's index in T
     std::vector<int32_t> bbucket;   // first edge (side-local) whose umax > bucket start
+    // compact walk table (shared-memory staged walk, see kCompact* below); empty
+    // when the mesh exceeds the compact word limits
+    std::vector<uint32_t> crec;     // 2 per record 3N+j (+ pad to 16 B)
+    std::vector<double> vxy;        // 2 per vertex
 };
+
+// Compact walk table (K4 shared-memory variant).  Record 3N+j is 8 bytes:
+//   .x = cw(word of edge (j+1)%3) | vid(corner j) << 18
+//   .y = cw(word of edge (j+2)%3)
+// with the vertex coordinates in a separate vxy[V] table (16 B per vertex).
+// Compact words: internal edges keep their record index 3n+j (< 2^17);
+// stop words are bit 17 | boundary kind at bit 16 | segment id (< 0xFFFF);
+// 0x3FFFF is the open word.  For Lines-1024 (4,050 triangles, 2,052
+// vertices) the table is 97 KB + 33 KB and lives in shared memory; a step then
+// reads 8 + 16 bytes from shared memory and never misses.
+constexpr uint32_t kCStop = 1u << 17;
+constexpr uint32_t kCBoundary = 1u << 16;
+constexpr uint32_t kCOpen = 0x3FFFFu;
+constexpr uint32_t kCWordMask = 0x3FFFFu;
+constexpr int kCVidShift = 18;
+constexpr int kSmemWalkMax = 200 * 1024;  // staged only if the table fits this
 
 // Build the packed layout; returns MWT_OK or an error code with *err set.
 int pack_mesh(const double *vx, const double *vy, int32_t nverts, const int32_t *tri_v,
@@ -106,6 +126,11 @@ struct MeshDev {
     const double4 *bpq;     // (P.x, P.y, Q.x, Q.y) per edge
     const int32_t *bword;
     const int32_t *bbucket;
+    // compact walk table for the shared-memory staged walk (NULL if absent)
+    const uint2 *crec;
+    const double2 *vxy;
+    int32_t crec_bytes;  // 16-B padded size of crec; vxy follows it in shared memory
+    int32_t smem_bytes;  // crec_bytes + 16 * nv if the table fits kSmemWalkMax, else 0
     // a device-memory copy of this struct, for out-of-line device functions
     // (passing the kernel-parameter copy by reference would force it into
     // local memory)

@@ -143,6 +143,28 @@ int pack_mesh(const double *vx, const double *vy, int32_t nv, const int32_t *tv,
             r[1] = P.link[4LL * t + (j + 2) % 3];
             std::memcpy(r + 4, &P.cxy[6LL * t + 2 * j], 16);
         }
+    // compact walk table (same record indices, vertex-indexed apex)
+    if (3LL * nt < (1LL << 17) && nv < (1 << 14) && ns < 0xFFFF) {
+        auto cw = [](uint32_t w) -> uint32_t {
+            if (!(w & kStopBit)) return w;
+            if (w == kOpenWord) return kCOpen;
+            return kCStop | ((w & kBoundaryBit) ? kCBoundary : 0u) | (w & kSidMask);
+        };
+        const int64_t nrec = 3LL * nt, padded = (nrec + 1) & ~1LL;
+        P.crec.assign(2 * padded, 0u);
+        for (int t = 0; t < nt; t++)
+            for (int j = 0; j < 3; j++) {
+                const int64_t k = 3LL * t + j;
+                P.crec[2 * k] = cw((uint32_t)P.link[4LL * t + (j + 1) % 3]) |
+                                ((uint32_t)tv[3 * t + j] << kCVidShift);
+                P.crec[2 * k + 1] = cw((uint32_t)P.link[4LL * t + (j + 2) % 3]);
+            }
+        P.vxy.resize(2LL * nv);
+        for (int v = 0; v < nv; v++) {
+            P.vxy[2LL * v] = vx[v];
+            P.vxy[2LL * v + 1] = vy[v];
+        }
+    }
     P.seg.assign(seg_xy, seg_xy + 4LL * ns);
     P.segkind.assign(seg_kind, seg_kind + ns);
 

@@ -217,8 +217,29 @@ struct WalkState {
 // the 32-B step record k (words of the two candidate exits, apex corner)
 __device__ __forceinline__ void load_step(const MeshDev &M, uint32_t k, int4 &W, double2 &A) {
     const int4 *p = M.step + 2 * (size_t)k;
-    W = __ldg(p);
-    A = __ldg(reinterpret_cast<const double2 *>(p + 1));
+    unsigned long long w01, w23;
+    asm("ld.global.nc.v4.b64 {%0, %1, %2, %3}, [%4];"
+        : "=l"(w01), "=l"(w23), "=d"(A.x), "=d"(A.y)
+        : "l"(p));
+    W.x = (int)(uint32_t)w01;
+    W.y = (int)(uint32_t)(w01 >> 32);
+    W.z = (int)(uint32_t)w23;
+    W.w = (int)(uint32_t)(w23 >> 32);
+}
+
+// the same record as ONE 256-bit load (sm_100 LDG.E.ENL2.256: one L1
+// wavefront per lane instead of two); volatile, so it is issued before the side
+// test rather than sunk into the branch that consumes the words
+__device__ __forceinline__ void load_step_issue(const MeshDev &M, uint32_t k, int4 &W, double2 &A) {
+    const int4 *p = M.step + 2 * (size_t)k;
+    unsigned long long w01, w23;
+    asm volatile("ld.global.nc.v4.b64 {%0, %1, %2, %3}, [%4];"
+                 : "=l"(w01), "=l"(w23), "=d"(A.x), "=d"(A.y)
+                 : "l"(p));
+    W.x = (int)(uint32_t)w01;
+    W.y = (int)(uint32_t)(w01 >> 32);
+    W.z = (int)(uint32_t)w23;
+    W.w = (int)(uint32_t)(w23 >> 32);
 }
 
 // first triangle: edges 0 (s1,s2), 1 (s2,s0), 2 (s0,s1) in order, none skipped
@@ -451,9 +472,15 @@ struct TraceOut {
     uint32_t *st;
 };
 
-// Per-ray prologue (raygen or load, locate, first triangle), out of line so
-// its temporaries do not inflate the walk loop's register budget; it runs in
-// refill batches, many lanes at once.
+// Per-launch constants: one __grid_constant__ kernel parameter.  The
+// out-of-line prologue and epilogue take its address, so they cost neither
+// argument registers nor a local copy.
+struct Launch {
+    RaySrc src;
+    TraceOut out;
+};
+
+// Per-ray prologue result (raygen or load, locate, first triangle)
 struct Init {
     double ox, oy, dx, dy, sp, sq;
     uint32_t w, st;
@@ -512,18 +539,7 @@ __device__ __forceinline__ bool boundary_start(const MeshDev &M, const Ray &r, W
 }
 
 template <bool GEN>
-__device__ __noinline__ Init prologue(long long i, int mode, double bx0, double by0, double bx1,
-                                      double by1, unsigned long long key, unsigned long long first,
-                                      const double *rays, const int32_t *start,
-                                      const MeshDev *__restrict__ Mg) {
-    const MeshDev &M = *Mg;
-    RaySrc src{};
-    src.mode = mode;
-    src.box = Box{bx0, by0, bx1, by1};
-    src.key = key;
-    src.first = first;
-    src.rays = rays;
-    src.start = start;
+__device__ __forceinline__ Init prologue_body(const MeshDev &M, const RaySrc &src, long long i) {
     Init o;
     o.st = 0;
     const Ray r = GEN ? gen_ray(src.mode, src.box, src.key, src.first + (unsigned long long)i)
@@ -571,240 +587,254 @@ __device__ __noinline__ Init prologue(long long i, int mode, double bx0, double 
     return o;
 }
 
-template <bool GEN, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB)
-    k_trace(MeshDev M, const MeshDev *__restrict__ Mg, RaySrc src, long long n, TraceOut out,
+// Out of line (its temporaries stay out of the walk loop's register budget);
+// it runs in refill batches, many lanes at once.  Returns the state packed:
+// flags = phase | fast << 2 | ch << 3 | steps << 4 (steps is 0 or 1 here).
+struct InitP {
+    double ox, oy, dx, dy, sp, sq;
+    uint32_t w, st;
+    int kr;
+    uint32_t flags;
+};
+
+template <bool GEN>
+__device__ __noinline__ InitP prologue(long long i, const Launch *__restrict__ L,
+                                       const MeshDev *__restrict__ Mg) {
+    const Init in = prologue_body<GEN>(*Mg, L->src, i);
+    if (L->out.start) L->out.start[i] = in.start;
+    InitP o;
+    o.ox = in.ox; o.oy = in.oy; o.dx = in.dx; o.dy = in.dy; o.sp = in.sp; o.sq = in.sq;
+    o.w = in.w; o.st = in.st; o.kr = in.cur;
+    o.flags = (uint32_t)in.phase | (in.fast ? 4u : 0u) | ((uint32_t)in.ei << 3) | ((uint32_t)in.steps << 4);
+    return o;
+}
+
+// Block-private histogram with warp-aggregated updates: one shared atomic per
+// distinct step bin in the warp, one per hit / miss / status bit present.
+struct HistSm {
+    unsigned int bins[MWT_HIST_LEN];
+    unsigned long long steps_sum;
+};
+
+__device__ __forceinline__ void hist_add_warp(HistSm *H, int seg, int steps, uint32_t st) {
+    const unsigned m = __activemask();
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    const int bin = steps < MWT_HIST_STEP_BINS - 1 ? (steps < 0 ? 0 : steps) : MWT_HIST_STEP_BINS - 1;
+    const unsigned same = __match_any_sync(m, bin);
+    if (lane == __ffs(same) - 1) atomicAdd(H->bins + bin, (unsigned)__popc(same));
+    const unsigned hits = __ballot_sync(m, seg >= 0);
+    const unsigned ssum = __reduce_add_sync(m, (unsigned)(steps > 0 ? steps : 0));
+    unsigned any = __reduce_or_sync(m, st) & 0xFFFu;
+    if (lane == leader) {
+        if (hits) atomicAdd(H->bins + MWT_HIST_HIT, (unsigned)__popc(hits));
+        if (m & ~hits) atomicAdd(H->bins + MWT_HIST_MISS, (unsigned)__popc(m & ~hits));
+        atomicAdd(&H->steps_sum, (unsigned long long)ssum);
+    }
+    while (any) {
+        const int b = __ffs(any) - 1;
+        any &= any - 1;
+        const unsigned c = __ballot_sync(m, (st >> b) & 1u);
+        if (lane == leader) atomicAdd(H->bins + MWT_HIST_STATUS0 + b, (unsigned)__popc(c));
+    }
+}
+
+// Out-of-line epilogue for a lane whose ray has ended (phase 2: exit edge
+// reached; phase 3: TraversalError): hit test, per-ray outputs, histogram.
+__device__ __noinline__ void epilogue(const MeshDev *__restrict__ Mg, const Launch *__restrict__ L,
+                                      HistSm *H, long long i, double ox, double oy, double dx,
+                                      double dy, int kr, int ch, uint32_t w, double sp, double sq,
+                                      uint32_t st, int steps, int phase) {
+    int seg = -1;
+    double t = CUDART_NAN, u = CUDART_NAN;
+    if (phase == 2) {
+        const Ray r{ox, oy, dx, dy};
+        WalkState s;
+        s.kr = kr;
+        s.ch = ch;
+        s.w = w;
+        s.sp = sp;
+        s.sq = sq;
+        seg = walk_terminal(*Mg, r, s, t, u, st);
+    }
+    const TraceOut &O = L->out;
+    if (O.seg) O.seg[i] = seg;
+    if (O.t) O.t[i] = t;
+    if (O.u) O.u[i] = u;
+    if (O.steps) O.steps[i] = steps;
+    if (O.st) O.st[i] = st;
+    if (H) hist_add_warp(H, seg, steps, st);
+}
+
+// compact stop word (shared-memory table) -> full walk word
+__device__ __forceinline__ uint32_t expand_cword(uint32_t c) {
+    if (c == kCOpen) return kOpenWord;
+    return kStopBit | ((c & kCBoundary) ? kBoundaryBit : 0u) | (c & 0xFFFFu);
+}
+
+constexpr int kGrab = 256;  // rays a warp takes from its CTA's counter at a time
+
+// The trace kernel.  Each CTA owns a contiguous range of rays; its warps take
+// kGrab rays at a time from a shared counter (so all warps of a CTA finish
+// together), and each warp keeps its lanes busy: once at most `refill_below`
+// lanes are still walking, the lanes whose rays ended run the epilogue and
+// the idle lanes the prologue of the next rays, both as one batch.
+//
+// SMEM: the compact walk table (mwt_internal.h) is staged into shared memory
+// once per CTA and the tight loop reads it there (one CTA of THREADS per SM);
+// otherwise the tight loop reads the 32-B step records from global memory.
+template <bool GEN, int MINB, int THREADS, bool SMEM>
+__global__ void __launch_bounds__(THREADS, MINB)
+    k_trace(const __grid_constant__ MeshDev M, const __grid_constant__ Launch L, long long n,
             long long *hist, int refill_below) {
-    __shared__ unsigned int h[MWT_HIST_LEN];
-    if (hist) hist_init(h);
+    __shared__ HistSm H;
+    __shared__ unsigned long long s_next;
+    extern __shared__ __align__(16) unsigned char dsm[];
+    const uint2 *srec = reinterpret_cast<const uint2 *>(dsm);
+    const double2 *svxy = reinterpret_cast<const double2 *>(dsm + (SMEM ? M.crec_bytes : 0));
+    if (SMEM) {
+        const int n16 = M.smem_bytes >> 4, c16 = M.crec_bytes >> 4;
+        uint4 *d = reinterpret_cast<uint4 *>(dsm);
+        const uint4 *a = reinterpret_cast<const uint4 *>(M.crec);
+        const uint4 *b = reinterpret_cast<const uint4 *>(M.vxy);
+        for (int k = threadIdx.x; k < n16; k += THREADS) d[k] = k < c16 ? __ldg(a + k) : __ldg(b + (k - c16));
+    }
+    const long long per = (n + gridDim.x - 1) / gridDim.x;
+    const long long cbeg = (long long)blockIdx.x * per;
+    const long long cend = cbeg + per < n ? cbeg + per : n;
+    if (hist)
+        for (int k = threadIdx.x; k < MWT_HIST_LEN; k += THREADS) H.bins[k] = 0u;
+    if (threadIdx.x == 0) {
+        H.steps_sum = 0ull;
+        s_next = (unsigned long long)cbeg;
+    }
+    __syncthreads();
+    HistSm *Hp = hist ? &H : nullptr;
+    const MeshDev *Mg = M.self;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
-    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-    const long long chunk = (n + nwarps - 1) / nwarps;
-    long long next = warp * chunk;
-    const long long end = next + chunk < n ? next + chunk : n;
-    unsigned long long steps_sum = 0;
+    const int lim = 4 * M.nt + 16;  // walk_step's guard
+    long long next = 0, end = 0;    // the warp's current grab
+    bool more = cbeg < cend;        // warp-uniform: the CTA range is not exhausted
 
-    // lane phase: 0 idle, 1 walking, 2 reached its exit edge (terminal pending),
-    // 3 failed (TraversalError pending).  Terminals are resolved in batches at
-    // refill time so the once-per-ray epilogue also runs with many lanes.
+    // lane phase: 0 idle, 1 walking, 2 reached its exit edge (epilogue pending),
+    // 3 failed (TraversalError pending)
     int phase = 0;
     long long idx = 0;
-    Ray r;
+    Ray r{0.0, 0.0, 0.0, 0.0};
     WalkState s;
+    s.kr = 0; s.ch = 0; s.steps = 0; s.w = 0; s.sp = 0.0; s.sq = 0.0; s.fast = false;
     uint32_t st = 0;
 
     while (true) {
         unsigned walking = __ballot_sync(FULL, phase == 1);
         if (__popc(walking) <= refill_below) {
-            // epilogue batch: resolve every pending lane
             if (phase >= 2) {
-                int seg = -1;
-                double t = CUDART_NAN, u = CUDART_NAN;
-                if (phase == 2) {
-                    const Term tm = terminal(M.seg, M.ep_range, M.ep_ids, M.cxy, r.ox, r.oy, r.dx,
-                                             r.dy, s.kr, s.ch, s.w, s.sp, s.sq, st);
-                    seg = tm.seg;
-                    t = tm.t;
-                    u = tm.u;
-                    st = tm.st;
-                }
-                if (out.seg) out.seg[idx] = seg;
-                if (out.t) out.t[idx] = t;
-                if (out.u) out.u[idx] = u;
-                if (out.steps) out.steps[idx] = s.steps;
-                if (out.st) out.st[idx] = st;
-                if (hist) {
-                    hist_add(h, seg, s.steps, st);
-                    steps_sum += (unsigned long long)s.steps;
-                }
+                epilogue(Mg, &L, Hp, idx, r.ox, r.oy, r.dx, r.dy, s.kr, s.ch, s.w, s.sp, s.sq, st,
+                         s.steps, phase);
                 phase = 0;
             }
-            // prologue batch: idle lanes take the next rays of the chunk
-            if (next < end) {
+            if (more) {
                 const unsigned idle = ~walking;
+                const int nidle = __popc(idle), rank = __popc(idle & lt_mask);
+                // rays for the idle lanes: the rest of the current grab, then a new one
+                long long nb = end, ne = end;
+                const int rem = (int)(end - next);
+                if (rem < nidle) {
+                    unsigned long long base = 0;
+                    if (lane == 0) base = atomicAdd(&s_next, (unsigned long long)kGrab);
+                    base = __shfl_sync(FULL, base, 0);
+                    nb = (long long)base;
+                    ne = nb + kGrab < cend ? nb + kGrab : cend;
+                    if (nb >= cend) nb = ne = cend;
+                }
                 if (phase == 0) {
-                    const long long i = next + __popc(idle & lt_mask);
-                    if (i < end) {
+                    const long long i = rank < rem ? next + rank : nb + (rank - rem);
+                    if (rank < rem || i < ne) {
                         idx = i;
-                        const Init in = prologue<GEN>(
-                            i, src.mode, src.box.x0, src.box.y0, src.box.x1, src.box.y1, src.key,
-                            src.first, src.rays, src.start, Mg);
+                        const InitP in = prologue<GEN>(i, &L, Mg);
                         r.ox = in.ox; r.oy = in.oy; r.dx = in.dx; r.dy = in.dy;
-                        s.sp = in.sp; s.sq = in.sq; s.w = in.w;
-                        s.kr = in.cur; s.ch = in.ei; s.steps = in.steps;
-                        s.fast = in.fast;
+                        s.sp = in.sp; s.sq = in.sq; s.w = in.w; s.kr = in.kr;
                         st = in.st;
-                        phase = in.phase;
-                        if (out.start) out.start[i] = in.start;
+                        phase = (int)(in.flags & 3u);
+                        s.fast = (in.flags & 4u) != 0;
+                        s.ch = (int)((in.flags >> 3) & 1u);
+                        s.steps = (int)(in.flags >> 4);
                     }
                 }
-                next += __popc(idle);
+                if (rem >= nidle) {
+                    next += nidle;
+                } else {
+                    next = nb + (nidle - rem) < ne ? nb + (nidle - rem) : ne;
+                    end = ne;
+                    more = next < end || ne < cend;
+                }
             }
             walking = __ballot_sync(FULL, phase == 1);
             if (walking == 0) {
-                if (next >= end && __ballot_sync(FULL, phase != 0) == 0) break;
+                if (!more && __ballot_sync(FULL, phase != 0) == 0) break;
                 continue;  // pending lanes resolve at the top of the loop
             }
         }
-        // several steps per refill check: amortises the ballot / refill bookkeeping
+        // Fast steps in a tight loop: lanes in the one-candidate state (see
+        // walk_step) step until too few remain to keep the warp busy -- or,
+        // once the range is exhausted, until none remains.  A lane leaves on a
+        // zero apex side (the general rule decides that step), at its stop
+        // edge, or at the step guard (walk_step below flags the error).
+        {
+            const int thr = more ? refill_below : 0;
+            bool fl = phase == 1 && s.fast && s.steps < lim;
+            while (__popc(__ballot_sync(FULL, fl)) > thr) {
 #pragma unroll
-        for (int u2 = 0; u2 < 2; u2++) {
-            if (phase == 1) {
-                if (!walk_step(M, r, s, st)) phase = 3;
-                else if (s.w & kStopBit) phase = 2;
-            }
-        }
-    }
-    if (hist) hist_flush(h, steps_sum, hist);
-}
-
-// ---------------------------------------------------------------------------
-// Queue variant (default).  Each warp keeps two 32-entry lane-state queues in
-// shared memory.  Prologues run in bulk -- all 32 lanes prepare the next 32
-// rays of the warp's chunk (raygen / load, locate, first triangle) into the
-// prologue queue -- and walking lanes that go idle pop a prepared ray every
-// iteration, so walk steps run with nearly all lanes busy.  Rays that reach
-// their exit edge park in the epilogue queue; when it would overflow, all
-// lanes resolve the parked rays together (hit test, canonical, writes).
-
-struct LaneQ {  // SoA, one entry per lane slot
-    double ox[32], oy[32], dx[32], dy[32], sp[32], sq[32];
-    long long idx[32];
-    uint32_t w[32], st[32];
-    int cur[32], ei[32], steps[32];
-    unsigned char phase[32], fast[32];
-};
-
-template <bool GEN, int MINB>
-__global__ void __launch_bounds__(kThreads, MINB)
-    k_trace_q(MeshDev M, const MeshDev *__restrict__ Mg, RaySrc src, long long n, TraceOut out,
-              long long *hist) {
-    __shared__ unsigned int h[MWT_HIST_LEN];
-    __shared__ LaneQ qs[2 * (kThreads / 32)];
-    if (hist) hist_init(h);
-    const unsigned FULL = 0xffffffffu;
-    const int lane = threadIdx.x & 31;
-    const unsigned lt_mask = (1u << lane) - 1u;
-    LaneQ &PQ = qs[2 * (threadIdx.x >> 5)];
-    LaneQ &EQ = qs[2 * (threadIdx.x >> 5) + 1];
-    const long long warp = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const long long nwarps = ((long long)gridDim.x * blockDim.x) >> 5;
-    const long long chunk = (n + nwarps - 1) / nwarps;
-    long long next = warp * chunk;
-    const long long end = next + chunk < n ? next + chunk : n;
-    unsigned long long steps_sum = 0;
-    int pro_h = 0, pro_n = 0, epi_n = 0;  // warp-uniform queue cursors
-
-    int phase = 0;  // 0 idle, 1 walking, 2 exit edge reached, 3 failed
-    long long idx = 0;
-    Ray r;
-    WalkState s;
-    uint32_t st = 0;
-
-    // all lanes: resolve the first cnt parked rays of EQ
-    auto bulk_epilogue = [&](int cnt) {
-        if (lane < cnt) {
-            const int k = lane;
-            const int seg0 = -1;
-            int seg = seg0;
-            double t = CUDART_NAN, u = CUDART_NAN;
-            uint32_t est = EQ.st[k];
-            if (EQ.phase[k] == 2) {
-                const Term tm = terminal(M.seg, M.ep_range, M.ep_ids, M.cxy, EQ.ox[k], EQ.oy[k],
-                                         EQ.dx[k], EQ.dy[k], EQ.cur[k], EQ.ei[k], EQ.w[k], EQ.sp[k],
-                                         EQ.sq[k], est);
-                seg = tm.seg;
-                t = tm.t;
-                u = tm.u;
-                est = tm.st;
-            }
-            const long long q = EQ.idx[k];
-            const int nst = EQ.steps[k];
-            if (out.seg) out.seg[q] = seg;
-            if (out.t) out.t[q] = t;
-            if (out.u) out.u[q] = u;
-            if (out.steps) out.steps[q] = nst;
-            if (out.st) out.st[q] = est;
-            if (hist) {
-                hist_add(h, seg, nst, est);
-                steps_sum += (unsigned long long)nst;
-            }
-        }
-        __syncwarp();
-    };
-
-    while (true) {
-        // parked lanes -> epilogue queue
-        const unsigned pend = __ballot_sync(FULL, phase >= 2);
-        if (pend) {
-            if (epi_n + __popc(pend) > 32) {
-                bulk_epilogue(epi_n);
-                epi_n = 0;
-            }
-            if (phase >= 2) {
-                const int k = epi_n + __popc(pend & lt_mask);
-                EQ.ox[k] = r.ox; EQ.oy[k] = r.oy; EQ.dx[k] = r.dx; EQ.dy[k] = r.dy;
-                EQ.sp[k] = s.sp; EQ.sq[k] = s.sq; EQ.idx[k] = idx; EQ.w[k] = s.w; EQ.st[k] = st;
-                EQ.cur[k] = s.kr; EQ.ei[k] = s.ch; EQ.steps[k] = s.steps;
-                EQ.phase[k] = (unsigned char)phase;
-                phase = 0;
-            }
-            epi_n += __popc(pend);
-            __syncwarp();
-        }
-        // idle lanes <- prologue queue (bulk refill when exhausted)
-        const unsigned idle = __ballot_sync(FULL, phase == 0);
-        if (idle) {
-            if (pro_h == pro_n && next < end) {
-                const long long i = next + lane;
-                if (i < end) {
-                    const Init in = prologue<GEN>(
-                        i, src.mode, src.box.x0, src.box.y0, src.box.x1, src.box.y1, src.key,
-                        src.first, src.rays, src.start, Mg);
-                    PQ.ox[lane] = in.ox; PQ.oy[lane] = in.oy; PQ.dx[lane] = in.dx; PQ.dy[lane] = in.dy;
-                    PQ.sp[lane] = in.sp; PQ.sq[lane] = in.sq; PQ.idx[lane] = i; PQ.w[lane] = in.w;
-                    PQ.st[lane] = in.st; PQ.cur[lane] = in.cur; PQ.ei[lane] = in.ei;
-                    PQ.steps[lane] = in.steps; PQ.phase[lane] = (unsigned char)in.phase;
-                    PQ.fast[lane] = in.fast ? 1 : 0;
-                    if (out.start) out.start[i] = in.start;
-                }
-                pro_h = 0;
-                pro_n = end - next < 32 ? (int)(end - next) : 32;
-                next += pro_n;
-                __syncwarp();
-            }
-            const int avail = pro_n - pro_h;
-            if (phase == 0) {
-                const int rank = __popc(idle & lt_mask);
-                if (rank < avail) {
-                    const int k = pro_h + rank;
-                    r.ox = PQ.ox[k]; r.oy = PQ.oy[k]; r.dx = PQ.dx[k]; r.dy = PQ.dy[k];
-                    s.sp = PQ.sp[k]; s.sq = PQ.sq[k]; idx = PQ.idx[k]; s.w = PQ.w[k]; st = PQ.st[k];
-                    s.kr = PQ.cur[k]; s.ch = PQ.ei[k]; s.steps = PQ.steps[k];
-                    s.fast = PQ.fast[k] != 0;
-                    phase = PQ.phase[k];
+                for (int u2 = 0; u2 < 2; u2++) {
+                    if (fl) {
+                        const uint32_t k = s.w;
+                        uint32_t wx, wy;
+                        double2 A;
+                        if (SMEM) {
+                            const uint2 X = srec[k];
+                            A = svxy[X.x >> kCVidShift];
+                            wx = X.x & kCWordMask;
+                            wy = X.y;
+                        } else {
+                            int4 W;
+                            load_step_issue(M, k, W, A);
+                            wx = (uint32_t)W.x;
+                            wy = (uint32_t)W.y;
+                        }
+                        const double c = side_of(r, A);
+                        // branch-free commit (c == 0: nothing changes, the lane leaves)
+                        const bool ok = c != 0.0, pos = c > 0.0;
+                        const uint32_t nw = pos ? wx : wy;
+                        s.steps += ok ? 1 : 0;
+                        s.kr = ok ? (int)k : s.kr;
+                        s.sq = pos ? c : s.sq;
+                        s.sp = (ok && !pos) ? c : s.sp;
+                        s.ch = ok ? (pos ? 0 : 1) : s.ch;
+                        s.w = ok ? nw : s.w;
+                        const bool stop = ok && (nw & (SMEM ? kCStop : kStopBit));
+                        phase = stop ? 2 : phase;
+                        fl = ok && !stop && s.steps < lim;
+                    }
                 }
             }
-            const int took = __popc(idle) < avail ? __popc(idle) : avail;
-            pro_h += took;
         }
-        const unsigned walking = __ballot_sync(FULL, phase == 1);
-        if (walking == 0) {
-            if (next >= end && pro_h == pro_n && __ballot_sync(FULL, phase != 0) == 0) {
-                if (epi_n) bulk_epilogue(epi_n);
-                break;
-            }
-            continue;
-        }
+        if (SMEM && (s.w & (kStopBit | kCStop)) == kCStop) s.w = expand_cword(s.w);
+        // one full-rule step for every lane still walking (zero sides, the
+        // general state, the guard, and the lanes the tight loop left behind)
         if (phase == 1) {
             if (!walk_step(M, r, s, st)) phase = 3;
             else if (s.w & kStopBit) phase = 2;
         }
     }
-    if (hist) hist_flush(h, steps_sum, hist);
+    if (hist) {
+        __syncthreads();
+        for (int k = threadIdx.x; k < MWT_HIST_LEN; k += THREADS)
+            if (H.bins[k] && k != MWT_HIST_STEPS_SUM)
+                atomicAdd(reinterpret_cast<unsigned long long *>(hist + k), (unsigned long long)H.bins[k]);
+        if (threadIdx.x == 0 && H.steps_sum)
+            atomicAdd(reinterpret_cast<unsigned long long *>(hist + MWT_HIST_STEPS_SUM), H.steps_sum);
+    }
 }
 
 __global__ void __launch_bounds__(kThreads) k_raygen(int mode, Box box, unsigned long long key,
@@ -853,59 +883,73 @@ __global__ void __launch_bounds__(kThreads) k_histogram(const int32_t *seg, cons
 #define MWT_LAUNCH_RET return (int)cudaGetLastError()
 
 static int g_refill_below = 4;  // tuned on B200 (tools/tune.py): refill late, walk long
-static int g_min_blocks = 3;   // 3: <= 80 regs (24 warps/SM), the measured best; 4: 64 regs; 2: no cap
-
-static int g_variant = 1;      // 1: refill kernel (k_trace, measured faster); 0: queue kernel (k_trace_q)
+static int g_min_blocks = 4;    // global-table variant: 4 CTAs x 256 threads (<= 64 regs)
+static int g_variant = 2;       // 2: shared-memory staged walk when the compact table fits, else 1
 
 template <typename K>
-static int persistent_grid(K kernel, long long n) {
-    // one resident wave: SMs x resident CTAs (cached per kernel and device)
-    static const void *keys[32];
-    static int devs[32], waves[32], nkeys = 0;
+static int persistent_grid(K kernel, long long n, int threads = kThreads, int smem = 0) {
+    // one resident wave: SMs x resident CTAs (cached per kernel, device, smem size)
+    static const void *keys[64];
+    static int devs[64], smems[64], waves[64], nkeys = 0;
     int dev = 0;
     cudaGetDevice(&dev);
     int wave = 0;
     for (int k = 0; k < nkeys; k++)
-        if (keys[k] == (const void *)kernel && devs[k] == dev) wave = waves[k];
+        if (keys[k] == (const void *)kernel && devs[k] == dev && smems[k] == smem) wave = waves[k];
     if (wave == 0) {
         int sms = 0, blocks_per_sm = 0;
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kernel, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kernel, threads, smem);
         if (blocks_per_sm <= 0) blocks_per_sm = 1;
         if (sms <= 0) sms = 148;
         wave = sms * blocks_per_sm;
-        if (nkeys < 32) {
+        if (nkeys < 64) {
             keys[nkeys] = (const void *)kernel;
             devs[nkeys] = dev;
+            smems[nkeys] = smem;
             waves[nkeys] = wave;
             nkeys++;
         }
     }
-    long long want = (n + kThreads - 1) / kThreads;
+    long long want = (n + threads - 1) / threads;
     return (int)(want < wave ? (want < 1 ? 1 : want) : wave);
 }
 
-template <bool GEN, int MINB>
-static void launch_k_trace(const MeshDev &m, const RaySrc &src, long long n, const TraceOut &out,
-                           long long *hist, void *stream) {
-    if (g_variant == 1) {
-        k_trace<GEN, MINB><<<persistent_grid(k_trace<GEN, MINB>, n), kThreads, 0,
-                             (cudaStream_t)stream>>>(m, m.self, src, n, out, hist, g_refill_below);
-    } else {
-        k_trace_q<GEN, MINB><<<persistent_grid(k_trace_q<GEN, MINB>, n), kThreads, 0,
-                               (cudaStream_t)stream>>>(m, m.self, src, n, out, hist);
+constexpr int kSmemThreads = 1024;  // one CTA per SM shares the staged table
+
+template <bool GEN, int MINB, int THREADS, bool SMEM>
+static bool launch_k_trace(const MeshDev &m, const Launch &L, long long n, long long *hist,
+                           void *stream) {
+    auto kern = k_trace<GEN, MINB, THREADS, SMEM>;
+    const int dyn = SMEM ? m.smem_bytes : 0;
+    if (SMEM) {
+        if (dyn <= 0) return false;
+        int dev = 0;
+        cudaGetDevice(&dev);
+        static bool attr_set[2][64] = {};
+        if (dev < 0 || dev >= 64) return false;
+        if (!attr_set[GEN][dev]) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWalkMax) !=
+                cudaSuccess)
+                return false;
+            attr_set[GEN][dev] = true;
+        }
     }
+    kern<<<persistent_grid(kern, n, THREADS, dyn), THREADS, dyn, (cudaStream_t)stream>>>(
+        m, L, n, hist, g_refill_below);
+    return true;
 }
 
 template <bool GEN>
-static void launch_k_trace_any(const MeshDev &m, const RaySrc &src, long long n,
-                               const TraceOut &out, long long *hist, void *stream) {
+static void launch_k_trace_any(const MeshDev &m, const Launch &L, long long n, long long *hist,
+                               void *stream) {
+    if (g_variant == 2 && launch_k_trace<GEN, 1, kSmemThreads, true>(m, L, n, hist, stream)) return;
     if (g_min_blocks == 3)
-        launch_k_trace<GEN, 3>(m, src, n, out, hist, stream);
+        launch_k_trace<GEN, 3, kThreads, false>(m, L, n, hist, stream);
     else if (g_min_blocks == 2)
-        launch_k_trace<GEN, 2>(m, src, n, out, hist, stream);
+        launch_k_trace<GEN, 2, kThreads, false>(m, L, n, hist, stream);
     else
-        launch_k_trace<GEN, 4>(m, src, n, out, hist, stream);
+        launch_k_trace<GEN, 4, kThreads, false>(m, L, n, hist, stream);
 }
 
 int launch_raygen(int mode, const double *box, uint64_t seed, uint64_t first, int64_t n,
@@ -928,11 +972,11 @@ int launch_trace(const MeshDev &m, const double *rays, const int32_t *start, int
                  int32_t *o_start, int32_t *o_seg, double *o_t, double *o_u, int32_t *o_steps,
                  uint32_t *o_st, void *stream) {
     if (n <= 0) return 0;
-    RaySrc src{};
-    src.rays = rays;
-    src.start = start;
-    TraceOut out{o_start, o_seg, o_steps, o_t, o_u, o_st};
-    launch_k_trace_any<false>(m, src, n, out, nullptr, stream);
+    Launch L{};
+    L.src.rays = rays;
+    L.src.start = start;
+    L.out = TraceOut{o_start, o_seg, o_steps, o_t, o_u, o_st};
+    launch_k_trace_any<false>(m, L, n, nullptr, stream);
     MWT_LAUNCH_RET;
 }
 
@@ -940,13 +984,13 @@ int launch_trace_generated(const MeshDev &m, int mode, const double *box, uint64
                            uint64_t first, int64_t n, int32_t *o_seg, double *o_t,
                            int32_t *o_steps, long long *hist, void *stream) {
     if (n <= 0) return 0;
-    RaySrc src{};
-    src.mode = mode;
-    src.box = Box{box[0], box[1], box[2], box[3]};
-    src.key = ray_key(seed, mode);
-    src.first = first;
-    TraceOut out{nullptr, o_seg, o_steps, o_t, nullptr, nullptr};
-    launch_k_trace_any<true>(m, src, n, out, hist, stream);
+    Launch L{};
+    L.src.mode = mode;
+    L.src.box = Box{box[0], box[1], box[2], box[3]};
+    L.src.key = ray_key(seed, mode);
+    L.src.first = first;
+    L.out = TraceOut{nullptr, o_seg, o_steps, o_t, nullptr, nullptr};
+    launch_k_trace_any<true>(m, L, n, hist, stream);
     MWT_LAUNCH_RET;
 }
 
@@ -960,7 +1004,7 @@ int launch_histogram(const int32_t *seg, const int32_t *steps, const uint32_t *s
 void set_tuning(int refill_below, int min_blocks, int variant) {
     if (refill_below >= 0) g_refill_below = refill_below > 31 ? 31 : refill_below;
     if (min_blocks >= 2 && min_blocks <= 4) g_min_blocks = min_blocks;
-    if (variant == 0 || variant == 1) g_variant = variant;
+    if (variant == 1 || variant == 2) g_variant = variant;
 }
 
 }  // namespace mwt

@@ -102,12 +102,15 @@ def test_generated_kernel_equals_explicit_rays_and_histogram():
         assert np.array_equal(h2.cpu().numpy(), ref)
 
 
-@pytest.mark.parametrize("refill,minb,variant", [(0, 4, 1), (4, 3, 1), (16, 2, 1), (31, 4, 1), (0, 4, 0), (0, 3, 0), (0, 2, 0)])
-def test_tuning_knobs_do_not_change_results(refill, minb, variant):
+@pytest.mark.parametrize("cfg,refill,minb,variant", [
+    ("hair512", 0, 4, 1), ("hair512", 4, 3, 1), ("hair512", 16, 2, 1), ("hair512", 31, 4, 1),
+    ("hair512", 4, 4, 2),  # table too large for shared memory: falls back to variant 1
+    ("lines1024", 0, 4, 2), ("lines1024", 4, 4, 2), ("lines1024", 31, 4, 2), ("lines1024", 4, 4, 1)])
+def test_tuning_knobs_do_not_change_results(cfg, refill, minb, variant):
     from oracle import oracle as orc
     from paper_2112_05570_b200 import _lib
     from paper_2112_05570_b200.engine import DeviceMesh
-    paths = fixture_paths("hair512", "mwt")
+    paths = fixture_paths(cfg, "mwt")
     m, om = DeviceMesh.from_files(*paths), orc.Mesh.from_files(*paths)
     rays = orc.raygen(0, (0, 0, 1, 1), 2, 0, 50000)
     ref = om.trace(rays)
@@ -115,7 +118,7 @@ def test_tuning_knobs_do_not_change_results(refill, minb, variant):
     try:
         got = m.trace(rays)
     finally:
-        _lib.lib.mwt_set_tuning(4, 3, 1)
+        _lib.lib.mwt_set_tuning(4, 4, 2)  # the defaults
     for k in ("start", "seg", "steps"):
         assert np.array_equal(got[k], ref[k])
 
