@@ -587,9 +587,10 @@ __device__ __forceinline__ Init prologue_body(const MeshDev &M, const RaySrc &sr
     return o;
 }
 
-// Out of line (its temporaries stay out of the walk loop's register budget);
-// it runs in refill batches, many lanes at once.  Returns the state packed:
+// Runs in refill batches, many lanes at once.  Returns the state packed:
 // flags = phase | fast << 2 | ch << 3 | steps << 4 (steps is 0 or 1 here).
+// (Inlined: an out-of-line call saves and restores the caller's live
+// registers through local memory, ~140 B of L2 write traffic per ray.)
 struct InitP {
     double ox, oy, dx, dy, sp, sq;
     uint32_t w, st;
@@ -598,7 +599,7 @@ struct InitP {
 };
 
 template <bool GEN>
-__device__ __noinline__ InitP prologue(long long i, const Launch *__restrict__ L,
+__device__ __forceinline__ InitP prologue(long long i, const Launch *__restrict__ L,
                                        const MeshDev *__restrict__ Mg) {
     const Init in = prologue_body<GEN>(*Mg, L->src, i);
     if (L->out.start) L->out.start[i] = in.start;
@@ -638,9 +639,9 @@ __device__ __forceinline__ void hist_add_warp(HistSm *H, int seg, int steps, uin
     }
 }
 
-// Out-of-line epilogue for a lane whose ray has ended (phase 2: exit edge
+// Epilogue for a lane whose ray has ended (phase 2: exit edge
 // reached; phase 3: TraversalError): hit test, per-ray outputs, histogram.
-__device__ __noinline__ void epilogue(const MeshDev *__restrict__ Mg, const Launch *__restrict__ L,
+__device__ __forceinline__ void epilogue(const MeshDev *__restrict__ Mg, const Launch *__restrict__ L,
                                       HistSm *H, long long i, double ox, double oy, double dx,
                                       double dy, int kr, int ch, uint32_t w, double sp, double sq,
                                       uint32_t st, int steps, int phase) {
@@ -709,7 +710,6 @@ __global__ void __launch_bounds__(THREADS, MINB)
     }
     __syncthreads();
     HistSm *Hp = hist ? &H : nullptr;
-    const MeshDev *Mg = M.self;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         unsigned walking = __ballot_sync(FULL, phase == 1);
         if (__popc(walking) <= refill_below) {
             if (phase >= 2) {
-                epilogue(Mg, &L, Hp, idx, r.ox, r.oy, r.dx, r.dy, s.kr, s.ch, s.w, s.sp, s.sq, st,
+                epilogue(&M, &L, Hp, idx, r.ox, r.oy, r.dx, r.dy, s.kr, s.ch, s.w, s.sp, s.sq, st,
                          s.steps, phase);
                 phase = 0;
             }
@@ -752,7 +752,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     const long long i = rank < rem ? next + rank : nb + (rank - rem);
                     if (rank < rem || i < ne) {
                         idx = i;
-                        const InitP in = prologue<GEN>(i, &L, Mg);
+                        const InitP in = prologue<GEN>(i, &L, &M);
                         r.ox = in.ox; r.oy = in.oy; r.dx = in.dx; r.dy = in.dy;
                         s.sp = in.sp; s.sq = in.sq; s.w = in.w; s.kr = in.kr;
                         st = in.st;
@@ -883,7 +883,7 @@ __global__ void __launch_bounds__(kThreads) k_histogram(const int32_t *seg, cons
 #define MWT_LAUNCH_RET return (int)cudaGetLastError()
 
 static int g_refill_below = 4;  // tuned on B200 (tools/tune.py): refill late, walk long
-static int g_min_blocks = 4;    // global-table variant: 4 CTAs x 256 threads (<= 64 regs)
+static int g_min_blocks = 3;    // 3: 80 registers (variant 1: 3 CTAs x 256; variant 2: 768-thread CTA); 4: 64
 static int g_variant = 2;       // 2: shared-memory staged walk when the compact table fits, else 1
 
 template <typename K>
@@ -943,7 +943,11 @@ static bool launch_k_trace(const MeshDev &m, const Launch &L, long long n, long 
 template <bool GEN>
 static void launch_k_trace_any(const MeshDev &m, const Launch &L, long long n, long long *hist,
                                void *stream) {
-    if (g_variant == 2 && launch_k_trace<GEN, 1, kSmemThreads, true>(m, L, n, hist, stream)) return;
+    if (g_variant == 2) {
+        if (g_min_blocks == 3 ? launch_k_trace<GEN, 1, 768, true>(m, L, n, hist, stream)
+                              : launch_k_trace<GEN, 1, kSmemThreads, true>(m, L, n, hist, stream))
+            return;
+    }
     if (g_min_blocks == 3)
         launch_k_trace<GEN, 3, kThreads, false>(m, L, n, hist, stream);
     else if (g_min_blocks == 2)
