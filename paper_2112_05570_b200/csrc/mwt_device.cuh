@@ -168,8 +168,12 @@ __device__ __forceinline__ double u01(unsigned long long s0, unsigned long long 
 __device__ __forceinline__ void disk_try(unsigned long long s0, int a, double &x, double &y,
                                          double &r2) {
     const unsigned long long z = mix64(s0 + (unsigned long long)(a + 1) * kGolden);
-    x = 2.0 * ((double)(unsigned)(z >> 32) * 0x1p-32) - 1.0;
-    y = 2.0 * ((double)(unsigned)(z & 0xffffffffull) * 0x1p-32) - 1.0;
+    // x = 2 * (hi * 2^-32) - 1, built without an integer conversion: the double
+    // 2 + hi * 2^-31 has hi in its top mantissa bits, and subtracting 3 is exact
+    // (both forms are exact, so the bits agree with the host twins)
+    const unsigned hi = (unsigned)(z >> 32), lo = (unsigned)z;
+    x = __hiloint2double((int)(0x40000000u | (hi >> 12)), (int)(hi << 20)) - 3.0;
+    y = __hiloint2double((int)(0x40000000u | (lo >> 12)), (int)(lo << 20)) - 3.0;
     r2 = x * x + y * y;
 }
 
