@@ -179,6 +179,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu)")
+    ap.add_argument("--no-extra", action="store_true", help="skip per-config / like-for-like lines")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -301,6 +302,13 @@ def main():
     }
 
     line["clocks"] = clk.summary()
+    line["roofline"]["mesh_resident"] = (
+        f"shared memory ({mesh.info.walk_smem_bytes} B compact walk table staged per CTA); "
+        "HBM carries only per-ray output" if mesh.info.walk_smem_bytes > 0 else
+        "L2 (126 MB); HBM carries only per-ray output")
+    if rank == 0 and world == 1 and not args.profile and not args.no_extra:
+        line["per_config"] = per_config(local)
+        line["like_for_like"] = like_for_like(args.config, local)
 
     if not args.no_e2e and not args.profile:
         line["e2e"] = e2e(mesh, parts, box, rank, world, args, dev)
@@ -314,6 +322,84 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def _time_ms(fn, reps=5):
+    import torch
+    for _ in range(2):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def per_config(local, n=1 << 22):
+    """Fused trace (K2+K3+K4+K7) of n box-entry rays on every config's meshes:
+    rays/s, steps/ray and where the walk table lives (not the headline)."""
+    from paper_2112_05570_b200.engine import DeviceMesh, new_histogram, summarize_histogram
+    res = {}
+    for cfg, (box, _) in CONFIGS.items():
+        for which in ("mwt", "cdt"):
+            paths = fixture(cfg, which)
+            if not os.path.exists(paths[1]):
+                continue
+            m = DeviceMesh.from_files(*paths, device=local)
+            h = new_histogram(local)
+            ms = _time_ms(lambda: m.trace_generated_device(0, box, SEED, 0, n, outputs=True, hist=None))
+            m.trace_generated_device(0, box, SEED, 0, n, outputs=False, hist=h)
+            import torch
+            torch.cuda.synchronize()
+            hs = summarize_histogram(h)
+            res[f"{cfg}/{which}"] = {"rays": n, "ms": ms, "rays_per_s": n / (ms / 1e3),
+                                     "steps_per_ray": hs["steps_per_ray"],
+                                     "hit_fraction": hs["hits"] / max(1, hs["rays"]),
+                                     "triangles": m.info.num_triangles,
+                                     "walk_smem_bytes": int(m.info.walk_smem_bytes)}
+            del m
+    return res
+
+
+def like_for_like(cfg, local, n=1 << 22):
+    """The same n box-entry rays (loaded from HBM) through the MWT walk, the
+    reference-built SAH BVH and roped kd-tree (c_t chosen by the reference rule:
+    minimum total ops over the same rays, accel.py:845-862)."""
+    import torch
+    from paper_2112_05570_b200.engine import DeviceBvh, DeviceKd, DeviceMesh
+    from paper_2112_05570_b200.formats import load_structure
+    box = CONFIGS[cfg][0]
+    d = os.path.join(ROOT, "fixtures", "data", cfg)
+    mesh = DeviceMesh.from_files(*fixture(cfg, "mwt"), device=local)
+    rays = mesh.raygen_device(0, box, SEED, 0, n)
+    out = {}
+    ms = _time_ms(lambda: mesh.trace_device(rays, None, want=("seg", "t", "steps")))
+    o = mesh.trace_device(rays, None, want=("seg", "steps"))
+    out["mwt_walk"] = {"ms": ms, "rays_per_s": n / (ms / 1e3),
+                       "ops_per_ray": float(o["steps"].double().mean()), "ops": "tri_steps"}
+    for kind, cls in (("bvh", DeviceBvh), ("kd", DeviceKd)):
+        files = sorted(f for f in os.listdir(d) if f.startswith(kind + "_ct"))
+        if not files:
+            continue
+        best = None
+        for f in files:
+            st = cls(mesh, load_structure(os.path.join(d, f)))
+            r = st.trace_device(rays)
+            keys = ("node_tests", "prim_tests") if kind == "bvh" else ("nodes", "ropes", "prims")
+            ops = sum(float(r[k].double().sum()) for k in keys)
+            if best is None or ops < best[0]:
+                best = (ops, f, st)
+        ops, f, st = best
+        ms = _time_ms(lambda: st.trace_device(rays))
+        out[kind] = {"ms": ms, "rays_per_s": n / (ms / 1e3), "ops_per_ray": ops / n,
+                     "c_t": float(st.c_t), "file": f}
+    out["rays"] = f"{n} box-entry rays of {cfg}, loaded from HBM (32 B/ray in, seg/t/counters out)"
+    return out
 
 
 def e2e(mesh, parts, box, rank, world, args, dev):

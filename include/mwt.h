@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define MWT_ABI_VERSION 1
+#define MWT_ABI_VERSION 2
 
 /* return codes */
 #define MWT_OK 0
@@ -78,7 +78,9 @@ typedef struct {
     int32_t anchors_not_strict;    /* anchor centres on an edge/vertex (order-dependent seeds) */
     int32_t device;
     int64_t device_bytes;          /* total device footprint of the packed mesh */
-    int64_t walk_record_bytes;     /* bytes per triangle read by one walk step */
+    int64_t walk_record_bytes;     /* algorithmic bytes per triangle step (32) */
+    int64_t walk_smem_bytes;       /* compact walk table staged in shared memory per CTA
+                                      (0: walk records read from global memory) */
 } mwt_mesh_info;
 
 /* Library / error plumbing */

@@ -41,7 +41,7 @@ HIST_STEPS_SUM = 1026
 HIST_STATUS0 = 1027
 HIST_LEN = 1040
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class MwtError(RuntimeError):
@@ -52,7 +52,8 @@ class MeshInfo(ctypes.Structure):
     _fields_ = [("num_vertices", ctypes.c_int32), ("num_triangles", ctypes.c_int32),
                 ("num_segments", ctypes.c_int32), ("anchor_res", ctypes.c_int32),
                 ("anchors_not_strict", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("device_bytes", ctypes.c_int64), ("walk_record_bytes", ctypes.c_int64)]
+                ("device_bytes", ctypes.c_int64), ("walk_record_bytes", ctypes.c_int64),
+                ("walk_smem_bytes", ctypes.c_int64)]
 
 
 # (name, restype, argtypes); every symbol declared in include/mwt.h

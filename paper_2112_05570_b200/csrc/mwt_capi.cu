@@ -210,6 +210,7 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     m->info.device = device;
     m->info.device_bytes = (int64_t)bytes;
     m->info.walk_record_bytes = 32;
+    m->info.walk_smem_bytes = m->dev.smem_bytes;
     *out = m;
     return MWT_OK;
 }
