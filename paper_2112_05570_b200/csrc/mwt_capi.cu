@@ -59,8 +59,8 @@ T *carve(Arena &a, size_t count) {
 
 }  // namespace
 
-constexpr int kHostStreams = 3;
-constexpr int64_t kHostChunk = 1 << 20;  // rays per pipelined chunk of mwt_trace_host
+constexpr int kHostStreams = 4;
+constexpr int64_t kHostChunk = 1 << 19;  // rays per pipelined chunk of mwt_trace_host
 
 struct mwt_mesh {
     int device = 0;

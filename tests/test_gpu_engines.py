@@ -163,29 +163,39 @@ def test_edge_cases():
 
 def test_full_size_floorplan_properties():
     """2^26 box-entry rays (the FloorPlan config size): no error / overflow,
-    histogram totals consistent, and a 2^16 subsample bit-exact vs the oracle."""
+    histogram totals consistent with the per-ray outputs, four 2^24-ray shards
+    (the weak-scaling split) sum to the whole, and 4,096 rays spread over the
+    whole index range bit-exact vs the oracle."""
     import torch
     from oracle import oracle as orc
     from paper_2112_05570_b200.engine import DeviceMesh, new_histogram, summarize_histogram
     paths = fixture_paths("floorplan64", "mwt")
     m = DeviceMesh.from_files(*paths)
     n = 1 << 26
+    box = (0, 0, 1, 1)
     h = new_histogram()
-    out = m.trace_generated_device(0, (0, 0, 1, 1), 0, 0, n, outputs=True, hist=h)
+    out = m.trace_generated_device(0, box, 0, 0, n, outputs=True, hist=h)
     torch.cuda.synchronize()
     s = summarize_histogram(h)
     assert s["rays"] == n and s["hits"] + s["misses"] == n
     assert s["status"]["error"] == 0 and s["status"]["overflow"] == 0
     assert s["steps_sum"] == int(out["steps"].to(torch.int64).sum())
-    idx = np.sort(np.random.default_rng(0).choice(n, 1 << 16, replace=False))
+    assert s["hits"] == int((out["seg"] >= 0).sum())
+    shards = new_histogram()
+    for k in range(4):
+        m.trace_generated_device(0, box, 0, k << 24, 1 << 24, outputs=False, hist=shards)
+    torch.cuda.synchronize()
+    assert torch.equal(shards, h)
+    idx = np.sort(np.random.default_rng(0).choice(n, 4096, replace=False))
     om = orc.Mesh.from_files(*paths)
-    first = int(idx[0])
-    rays = np.concatenate([orc.raygen(0, (0, 0, 1, 1), 0, int(i), 1) for i in idx[:256]])
+    rays = np.concatenate([orc.raygen(0, box, 0, int(i), 1) for i in idx])
     ref = om.trace(rays)
-    got_seg = out["seg"][torch.from_numpy(idx[:256]).cuda()].cpu().numpy()
-    got_steps = out["steps"][torch.from_numpy(idx[:256]).cuda()].cpu().numpy()
-    assert np.array_equal(got_seg, ref["seg"]) and np.array_equal(got_steps, ref["steps"])
-    del first
+    sel = torch.from_numpy(idx).cuda()
+    assert np.array_equal(out["seg"][sel].cpu().numpy(), ref["seg"])
+    assert np.array_equal(out["steps"][sel].cpu().numpy(), ref["steps"])
+    t = out["t"][sel].cpu().numpy()
+    hit = ref["seg"] >= 0
+    assert np.array_equal(t[hit], ref["t"][hit])
 
 
 def test_drop_in_api_on_model_objects():
