@@ -672,7 +672,7 @@ __device__ __forceinline__ uint32_t expand_cword(uint32_t c) {
     return kStopBit | ((c & kCBoundary) ? kBoundaryBit : 0u) | (c & 0xFFFFu);
 }
 
-constexpr int kGrab = 256;  // rays a warp takes from its CTA's counter at a time
+constexpr int kGrab = 128;  // rays a warp takes from its CTA's counter at a time
 
 // The trace kernel.  Each CTA owns a contiguous range of rays; its warps take
 // kGrab rays at a time from a shared counter (so all warps of a CTA finish
@@ -786,7 +786,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             bool fl = phase == 1 && s.fast && s.steps < lim;
             while (__popc(__ballot_sync(FULL, fl)) > thr) {
 #pragma unroll
-                for (int u2 = 0; u2 < 2; u2++) {
+                for (int u2 = 0; u2 < 4; u2++) {
                     if (fl) {
                         const uint32_t k = s.w;
                         uint32_t wx, wy;
