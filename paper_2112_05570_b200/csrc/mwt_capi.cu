@@ -124,7 +124,7 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
                    Arena::align(P.ep_ids.size() * 4) + Arena::align(P.anchor.size() * 4) +
                    Arena::align(P.bu.size() * 8) + Arena::align(P.bpq.size() * 8) +
                    Arena::align(P.bword.size() * 4) + Arena::align(P.bbucket.size() * 4) +
-                   Arena::align(sizeof(mwt::MeshDev)) + Arena::align(P.crec.size() * 4) +
+                   Arena::align(P.crec.size() * 4) +
                    Arena::align(P.vxy.size() * 8);
     Arena a;
     CK(cudaMalloc(&a.base, bytes));
@@ -145,7 +145,6 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     double *bpq = carve<double>(a, P.bpq.size());
     int32_t *bword = carve<int32_t>(a, P.bword.size());
     int32_t *bbucket = carve<int32_t>(a, P.bbucket.size());
-    mwt::MeshDev *self = carve<mwt::MeshDev>(a, 1);
     uint32_t *crec = carve<uint32_t>(a, P.crec.size());
     double *vxy = carve<double>(a, P.vxy.size());
     cudaError_t e = cudaSuccess;
@@ -191,16 +190,6 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
         m->dev.crec_bytes = (int32_t)(P.crec.size() * 4);
         const int64_t sm = (int64_t)m->dev.crec_bytes + 16LL * P.nv;
         m->dev.smem_bytes = sm <= mwt::kSmemWalkMax ? (int32_t)sm : 0;
-    }
-    m->dev.self = self;
-    {
-        cudaError_t e2 = cudaMemcpy(self, &m->dev, sizeof(mwt::MeshDev), cudaMemcpyHostToDevice);
-        if (e2 != cudaSuccess) {
-            cudaStreamDestroy(m->stream);
-            cudaFree(a.base);
-            delete m;
-            return cuda_fail(e2, "mesh_create: descriptor upload");
-        }
     }
     m->info.num_vertices = P.nv;
     m->info.num_triangles = P.nt;

@@ -131,10 +131,6 @@ struct MeshDev {
     const double2 *vxy;
     int32_t crec_bytes;  // 16-B padded size of crec; vxy follows it in shared memory
     int32_t smem_bytes;  // crec_bytes + 16 * nv if the table fits kSmemWalkMax, else 0
-    // a device-memory copy of this struct, for out-of-line device functions
-    // (passing the kernel-parameter copy by reference would force it into
-    // local memory)
-    const MeshDev *self;
 };
 
 struct BvhDev {
