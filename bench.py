@@ -301,6 +301,20 @@ def main():
         "histogram": {k: hsum[k] for k in ("rays", "hits", "misses", "steps_sum", "status")},
     }
 
+    # full per-ray byte count of the box-entry launch
+    spr = hb["steps_sum"] / max(1, hb["rays"])
+    hitf = hb["hits"] / max(1, hb["rays"])
+    line["per_ray_bytes"] = {
+        "walk_steps": ALGO_BYTES_PER_STEP * spr, "first_triangle": 48.0,
+        "boundary_table": 40.0, "output": 16.0, "hit_segment": 32.0 * hitf, "input_ray": 0.0,
+        "total": ALGO_BYTES_PER_STEP * spr + 48.0 + 40.0 + 16.0 + 32.0 * hitf,
+        "note": "walk = 32 B x steps/ray (the roofline's algorithmic bytes); first triangle = "
+                "its three corners; boundary table = bucket word + edge extent + word; "
+                "output = seg + t + steps; rays are generated on device"}
+    ns = sorted(f for f in os.listdir(os.path.join(ROOT, "profiles")) if f.endswith("_ncu_stats.json"))
+    if ns:
+        with open(os.path.join(ROOT, "profiles", ns[-1])) as fh:
+            line["ncu"] = json.load(fh)
     line["clocks"] = clk.summary()
     line["roofline"]["mesh_resident"] = (
         f"shared memory ({mesh.info.walk_smem_bytes} B compact walk table staged per CTA); "

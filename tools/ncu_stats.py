@@ -1,0 +1,64 @@
+"""Condense one ncu --set full capture of the box-entry k_trace launch into the
+figures SURVEY.md 8d asks the bench to carry (instructions per ray and per
+step, branch efficiency, achieved L2 / DRAM GB/s, shared-memory wavefronts).
+
+usage: ncu_stats.py report.ncu-rep rays steps_sum > profiles/rNN_ncu_stats.json
+"""
+import csv
+import io
+import json
+import subprocess
+import sys
+
+rep, rays, steps = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(io.StringIO(raw)))
+hdr, units = rows[0], rows[1]
+rows = [r for r in rows[2:] if len(r) == len(hdr) and "k_trace" in r[hdr.index("Kernel Name")]]
+r = rows[0]
+
+
+def g(name):
+    if name not in hdr:
+        return None
+    v = r[hdr.index(name)].replace(",", "")
+    try:
+        return float(v)
+    except ValueError:
+        return None
+
+
+dur_s = g("gpu__time_duration.sum") * {"ns": 1e-9, "us": 1e-6, "usecond": 1e-6, "ms": 1e-3,
+                                       "msecond": 1e-3}.get(units[hdr.index("gpu__time_duration.sum")], 1e-9)
+inst = g("smsp__inst_executed.sum")
+lts = (g("lts__t_sectors.sum") or 0) * 32
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def gb(name):  # a byte count in bytes, whatever unit ncu printed
+    return g(name) * SCALE.get(units[hdr.index(name)], 1)
+
+
+dram = gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum")
+out = {
+    "report": rep.split("/")[-1],
+    "kernel": r[hdr.index("Kernel Name")][:80],
+    "duration_ms": dur_s * 1e3,
+    "rays": rays,
+    "triangle_steps": steps,
+    "warp_instructions": inst,
+    "warp_instructions_per_ray": inst / rays,
+    "warp_instructions_per_step": inst / steps,
+    "avg_active_lanes": g("smsp__thread_inst_executed_per_inst_executed.ratio"),
+    "branch_efficiency_pct": g("smsp__sass_average_branch_targets_threads_uniform.pct"),
+    "issue_active_pct": g("sm__issue_active.avg.pct_of_peak_sustained_elapsed"),
+    "achieved_occupancy_pct": g("sm__warps_active.avg.pct_of_peak_sustained_active"),
+    "l2_gbs": lts / dur_s / 1e9 if lts else None,
+    "dram_gbs": dram / dur_s / 1e9,
+    "dram_bytes": dram,
+    "smem_wavefronts": g("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
+    "smem_bank_conflicts": g("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
+    "local_memory_instructions": (g("sass__inst_executed_local_loads") or 0) +
+    (g("sass__inst_executed_local_stores") or 0),
+}
+print(json.dumps(out, indent=1))
