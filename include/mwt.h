@@ -145,6 +145,14 @@ int mwt_locate_dev(const mwt_mesh *mesh, const double *pts, int64_t n, int32_t *
 int mwt_trace_dev(const mwt_mesh *mesh, const double *rays, const int32_t *start, int64_t n,
                   int32_t *out_start, int32_t *out_seg, double *out_t, double *out_u,
                   int32_t *out_steps, uint32_t *out_status, void *stream);
+/* K4 for chained (secondary) rays: as mwt_trace_dev, and out_end receives the
+ * triangle each walk ended in (the one whose exit edge is the hit segment or
+ * the boundary; -1 after a TraversalError).  Passing it back as the next ray's
+ * start replaces the locate (Ray.start_tri,
+ * geometry.py:66, consumed by traverse_triangulation, accel.py:138-160). */
+int mwt_trace_chain_dev(const mwt_mesh *mesh, const double *rays, const int32_t *start, int64_t n,
+                        int32_t *out_end, int32_t *out_seg, double *out_t, double *out_u,
+                        int32_t *out_steps, uint32_t *out_status, void *stream);
 /* Same as mwt_trace_dev on HOST buffers (copies in, traces, copies out, syncs). */
 int mwt_trace_host(const mwt_mesh *mesh, const double *rays, const int32_t *start, int64_t n,
                    int32_t *out_start, int32_t *out_seg, double *out_t, double *out_u,

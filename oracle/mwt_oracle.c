@@ -333,8 +333,11 @@ static inline double side_of(const orc_mesh *m, int vid, double ox, double oy, d
 }
 
 /* returns status; *seg = -1 on a miss */
+/* *end (may be NULL): the triangle the walk ended in -- the one whose exit
+ * edge is constrained or has no neighbour (the loop variable `cur` of
+ * accel.py:161-211 when it returns); -1 after a TraversalError */
 uint32_t orc_trace_one(const orc_mesh *m, const double ray[4], int start, int *seg, double *tout,
-                       double *uout, int *steps) {
+                       double *uout, int *steps, int *end) {
     double ox = ray[0], oy = ray[1], dx = ray[2], dy = ray[3];
     uint32_t st = 0;
     int cur = start;
@@ -398,6 +401,7 @@ uint32_t orc_trace_one(const orc_mesh *m, const double ray[4], int start, int *s
         cur = nxt;
     }
     *steps = nsteps;
+    if (end) *end = (st & ST_ERROR) ? -1 : cur;
     return st;
 }
 
@@ -596,8 +600,18 @@ void orc_locate(void *h, const double *pts, int64_t n, int32_t *out_tid, uint32_
 }
 
 /* start == NULL: locate each origin first (TriLocator.locate) */
+void orc_trace_ex(void *h, const double *rays, const int32_t *start, int64_t n, int32_t *out_start,
+                  int32_t *out_seg, double *out_t, double *out_u, int32_t *out_steps,
+                  uint32_t *out_st, int32_t *out_end);
+
 void orc_trace(void *h, const double *rays, const int32_t *start, int64_t n, int32_t *out_start,
                int32_t *out_seg, double *out_t, double *out_u, int32_t *out_steps, uint32_t *out_st) {
+    orc_trace_ex(h, rays, start, n, out_start, out_seg, out_t, out_u, out_steps, out_st, NULL);
+}
+
+void orc_trace_ex(void *h, const double *rays, const int32_t *start, int64_t n, int32_t *out_start,
+                  int32_t *out_seg, double *out_t, double *out_u, int32_t *out_steps,
+                  uint32_t *out_st, int32_t *out_end) {
     const orc_mesh *m = (const orc_mesh *)h;
 #pragma omp parallel for schedule(dynamic, 256)
     for (int64_t i = 0; i < n; i++) {
@@ -605,9 +619,11 @@ void orc_trace(void *h, const double *rays, const int32_t *start, int64_t n, int
         uint32_t st = 0;
         int s = start ? start[i] : orc_locate_one(m, r[0], r[1], &st);
         if (out_start) out_start[i] = s;
-        int seg, steps;
-        double t, u;
-        st |= orc_trace_one(m, r, s, &seg, &t, &u, &steps);
+        int seg = -1, steps = 0, end = -1;
+        double t = NAN, u = NAN;
+        if (s < 0 || s >= m->nt) st |= ST_ERROR; /* no such start triangle */
+        else st |= orc_trace_one(m, r, s, &seg, &t, &u, &steps, &end);
+        if (out_end) out_end[i] = end;
         out_seg[i] = seg;
         out_t[i] = t;
         if (out_u) out_u[i] = u;

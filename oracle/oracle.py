@@ -64,6 +64,7 @@ def lib():
         L.orc_anchors.argtypes = [P, P]
         L.orc_locate.argtypes = [P, P, i64, P, P]
         L.orc_trace.argtypes = [P, P, P, i64, P, P, P, P, P, P]
+        L.orc_trace_ex.argtypes = [P, P, P, i64, P, P, P, P, P, P, P]
         L.orc_brute_force.argtypes = [P, P, i64, P, P, P]
         L.orc_ray_segment_intersect.restype = ctypes.c_int
         L.orc_ray_segment_intersect.argtypes = [P, P, P, P]
@@ -205,13 +206,14 @@ class Mesh:
         rays = np.ascontiguousarray(rays, dtype=np.float64).reshape(-1, 4)
         n = len(rays)
         out = dict(start=np.empty(n, np.int32), seg=np.empty(n, np.int32), t=np.empty(n),
-                   u=np.empty(n), steps=np.empty(n, np.int32), status=np.empty(n, np.uint32))
+                   u=np.empty(n), steps=np.empty(n, np.int32), status=np.empty(n, np.uint32),
+                   end=np.empty(n, np.int32))
         sp = None
         if start is not None:
             start = np.ascontiguousarray(start, dtype=np.int32)
             sp = _p(start)
-        lib().orc_trace(self.h, _p(rays), sp, n, _p(out["start"]), _p(out["seg"]), _p(out["t"]),
-                        _p(out["u"]), _p(out["steps"]), _p(out["status"]))
+        lib().orc_trace_ex(self.h, _p(rays), sp, n, _p(out["start"]), _p(out["seg"]), _p(out["t"]),
+                           _p(out["u"]), _p(out["steps"]), _p(out["status"]), _p(out["end"]))
         return out
 
     def brute_force(self, rays: np.ndarray) -> dict:

@@ -72,6 +72,7 @@ SIGNATURES = {
     "mwt_raygen_dev": (INT, [INT, P, U64, U64, I64, P, P]),
     "mwt_locate_dev": (INT, [P, P, I64, P, P, P]),
     "mwt_trace_dev": (INT, [P, P, P, I64, P, P, P, P, P, P, P]),
+    "mwt_trace_chain_dev": (INT, [P, P, P, I64, P, P, P, P, P, P, P]),
     "mwt_trace_host": (INT, [P, P, P, I64, P, P, P, P, P, P]),
     "mwt_trace_generated_dev": (INT, [P, INT, P, U64, U64, I64, P, P, P, P, P]),
     "mwt_histogram_dev": (INT, [P, P, P, I64, P, P]),

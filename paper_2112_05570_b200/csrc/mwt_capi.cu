@@ -279,6 +279,18 @@ int mwt_trace_dev(const mwt_mesh *m, const double *rays, const int32_t *start, i
     return MWT_OK;
 }
 
+int mwt_trace_chain_dev(const mwt_mesh *m, const double *rays, const int32_t *start, int64_t n,
+                        int32_t *out_end, int32_t *out_seg, double *out_t, double *out_u,
+                        int32_t *out_steps, uint32_t *out_status, void *stream) {
+    if (!m || n < 0 || (n > 0 && !rays)) return fail(MWT_E_INVALID, "trace_chain: bad argument");
+    if (m->dev.nt == 0) return fail(MWT_E_INVALID, "trace_chain: mesh has no triangles");
+    DeviceGuard g(m->device);
+    int rc = mwt::launch_trace(m->dev, rays, start, n, nullptr, out_seg, out_t, out_u, out_steps,
+                               out_status, stream, out_end);
+    if (rc) return cuda_fail((cudaError_t)rc, "trace_chain launch");
+    return MWT_OK;
+}
+
 int mwt_trace_host(const mwt_mesh *cm, const double *rays, const int32_t *start, int64_t n,
                    int32_t *out_start, int32_t *out_seg, double *out_t, double *out_u,
                    int32_t *out_steps, uint32_t *out_status) {

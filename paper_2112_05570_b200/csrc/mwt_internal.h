@@ -160,7 +160,7 @@ int launch_locate(const MeshDev &m, const double *pts, int64_t n, int32_t *tid, 
                   void *stream);
 int launch_trace(const MeshDev &m, const double *rays, const int32_t *start, int64_t n,
                  int32_t *o_start, int32_t *o_seg, double *o_t, double *o_u, int32_t *o_steps,
-                 uint32_t *o_st, void *stream);
+                 uint32_t *o_st, void *stream, int32_t *o_end = nullptr);
 int launch_trace_generated(const MeshDev &m, int mode, const double *box, uint64_t seed,
                            uint64_t first, int64_t n, int32_t *o_seg, double *o_t,
                            int32_t *o_steps, long long *hist, void *stream);

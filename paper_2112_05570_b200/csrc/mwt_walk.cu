@@ -470,6 +470,7 @@ struct TraceOut {
     int32_t *start, *seg, *steps;
     double *t, *u;
     uint32_t *st;
+    int32_t *end;  // the triangle each walk ended in (-1 after an error)
 };
 
 // Per-launch constants: one __grid_constant__ kernel parameter.  The
@@ -663,6 +664,7 @@ __device__ __forceinline__ void epilogue(const MeshDev *__restrict__ Mg, const L
     if (O.u) O.u[i] = u;
     if (O.steps) O.steps[i] = steps;
     if (O.st) O.st[i] = st;
+    if (O.end) O.end[i] = phase == 2 ? kr / 3 : -1;
     if (H) hist_add_warp(H, seg, steps, st);
 }
 
@@ -974,12 +976,12 @@ int launch_locate(const MeshDev &m, const double *pts, int64_t n, int32_t *tid, 
 
 int launch_trace(const MeshDev &m, const double *rays, const int32_t *start, int64_t n,
                  int32_t *o_start, int32_t *o_seg, double *o_t, double *o_u, int32_t *o_steps,
-                 uint32_t *o_st, void *stream) {
+                 uint32_t *o_st, void *stream, int32_t *o_end) {
     if (n <= 0) return 0;
     Launch L{};
     L.src.rays = rays;
     L.src.start = start;
-    L.out = TraceOut{o_start, o_seg, o_steps, o_t, o_u, o_st};
+    L.out = TraceOut{o_start, o_seg, o_steps, o_t, o_u, o_st, o_end};
     launch_k_trace_any<false>(m, L, n, nullptr, stream);
     MWT_LAUNCH_RET;
 }
@@ -993,7 +995,7 @@ int launch_trace_generated(const MeshDev &m, int mode, const double *box, uint64
     L.src.box = Box{box[0], box[1], box[2], box[3]};
     L.src.key = ray_key(seed, mode);
     L.src.first = first;
-    L.out = TraceOut{nullptr, o_seg, o_steps, o_t, nullptr, nullptr};
+    L.out = TraceOut{nullptr, o_seg, o_steps, o_t, nullptr, nullptr, nullptr};
     launch_k_trace_any<true>(m, L, n, hist, stream);
     MWT_LAUNCH_RET;
 }

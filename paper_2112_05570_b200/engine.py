@@ -80,6 +80,13 @@ class DeviceMesh:
     def from_files(cls, scene_path: str, tri_path: str, device: int = 0) -> "DeviceMesh":
         return cls(load_scene(scene_path), load_tri(tri_path), device)
 
+    @classmethod
+    def from_binary(cls, path: str, device: int = 0) -> "DeviceMesh":
+        """A ``mwt-mesh v1`` directory (formats.save_mesh_binary)."""
+        from .formats import load_mesh_binary
+        scene, tri = load_mesh_binary(path)
+        return cls(scene, tri, device)
+
     @property
     def num_triangles(self) -> int:
         return self.info.num_triangles
@@ -123,6 +130,26 @@ class DeviceMesh:
         check(lib.mwt_trace_dev(self._h, ptr(rays), ptr(start.contiguous()) if start is not None else None,
                                 n, ptr(g("start")), ptr(g("seg")), ptr(g("t")), ptr(g("u")),
                                 ptr(g("steps")), ptr(g("status")), _stream(stream)), "trace")
+        return out
+
+    def trace_chain_device(self, rays: torch.Tensor, start: torch.Tensor | None = None,
+                           stream=None) -> dict:
+        """Walk and also return each walk's final triangle (``end``), to start
+        secondary rays there without a locate (mwt_trace_chain_dev)."""
+        rays = rays.contiguous()
+        n = rays.shape[0]
+        d = rays.device
+        out = dict(end=torch.empty(n, dtype=torch.int32, device=d),
+                   seg=torch.empty(n, dtype=torch.int32, device=d),
+                   t=torch.empty(n, dtype=torch.float64, device=d),
+                   u=torch.empty(n, dtype=torch.float64, device=d),
+                   steps=torch.empty(n, dtype=torch.int32, device=d),
+                   status=torch.empty(n, dtype=torch.int32, device=d))
+        check(lib.mwt_trace_chain_dev(self._h, ptr(rays),
+                                      ptr(start.contiguous()) if start is not None else None, n,
+                                      ptr(out["end"]), ptr(out["seg"]), ptr(out["t"]), ptr(out["u"]),
+                                      ptr(out["steps"]), ptr(out["status"]), _stream(stream)),
+              "trace_chain")
         return out
 
     def trace_generated_device(self, mode: int, box, seed: int, first: int, n: int,

@@ -5,6 +5,9 @@ input directly (numpy), plus the flattened kd-tree / BVH archives.
   mintri-tri v1     trimesh.py:1277-1337 (save_triangulation / load_triangulation)
   mwt-bvh v1 (.npz) flattened reference Bvh   (fixtures/gen_fixtures.py flatten_bvh)
   mwt-kd v1 (.npz)  flattened RopedKdTree     (fixtures/gen_fixtures.py flatten_kd)
+  mwt-mesh v1       binary SoA of a scene + triangulation: a
+                    directory of raw .npy arrays, memory-mapped on load -- the
+                    packer's input without text parsing
 
 Ids follow the files exactly: scene segments in file order (geometry first,
 then the four boundary sides, scene.py:5-6), triangles and vertices in the
@@ -173,3 +176,58 @@ def load_structure(path: str) -> dict:
     if fmt not in ("mwt-bvh v1", "mwt-kd v1"):
         raise FormatError(f"{path}: unknown structure format {fmt!r}")
     return out
+
+
+# ---------------------------------------------------------------------------
+# mwt-mesh v1: binary SoA (one .npy per array, memory-mappable)
+
+MESH_FORMAT = "mwt-mesh v1"
+_MESH_ARRAYS = {  # name: (dtype, columns)
+    "seg_xy": (np.float64, 4), "seg_kind": (np.uint8, 0),
+    "vxy": (np.float64, 2), "tri_v": (np.int32, 3), "tri_nbr": (np.int32, 3),
+    "tri_flag": (np.int32, 3),
+}
+
+
+def save_mesh_binary(path: str, scene: SceneArrays, tri: TriArrays) -> None:
+    """Write ``path/`` with format.txt and one .npy per SoA array."""
+    import json
+    import os
+    os.makedirs(path, exist_ok=True)
+    arrays = {"seg_xy": scene.xy, "seg_kind": scene.kind, "vxy": tri.vxy, "tri_v": tri.v,
+              "tri_nbr": tri.nbr, "tri_flag": tri.flag}
+    for name, (dt, cols) in _MESH_ARRAYS.items():
+        a = np.ascontiguousarray(arrays[name], dtype=dt)
+        if cols:
+            a = a.reshape(-1, cols)
+        np.save(os.path.join(path, name + ".npy"), a)
+    meta = {"format": MESH_FORMAT, "scene_name": scene.name, "num_segments": int(scene.num_segments),
+            "num_vertices": int(tri.num_vertices), "num_triangles": int(tri.num_triangles)}
+    with open(os.path.join(path, "format.txt"), "w") as fh:
+        fh.write(json.dumps(meta) + "\n")
+
+
+def load_mesh_binary(path: str, mmap: bool = True):
+    """Read a ``mwt-mesh v1`` directory: (SceneArrays, TriArrays), arrays
+    memory-mapped read-only when ``mmap``."""
+    import json
+    import os
+    try:
+        with open(os.path.join(path, "format.txt")) as fh:
+            meta = json.loads(fh.read())
+    except (OSError, ValueError) as e:
+        raise FormatError(f"{path}: not a {MESH_FORMAT} directory ({e})") from None
+    if meta.get("format") != MESH_FORMAT:
+        raise FormatError(f"{path}: unknown mesh format {meta.get('format')!r}")
+    a = {}
+    for name, (dt, cols) in _MESH_ARRAYS.items():
+        x = np.load(os.path.join(path, name + ".npy"), mmap_mode="r" if mmap else None)
+        if x.dtype != dt or (cols and (x.ndim != 2 or x.shape[1] != cols)):
+            raise FormatError(f"{path}/{name}.npy: expected {np.dtype(dt).name} with {cols} columns")
+        a[name] = x
+    if len(a["seg_xy"]) != meta["num_segments"] or len(a["tri_v"]) != meta["num_triangles"] or \
+            len(a["vxy"]) != meta["num_vertices"] or len(a["seg_kind"]) != meta["num_segments"]:
+        raise FormatError(f"{path}: array sizes disagree with format.txt")
+    scene = SceneArrays(a["seg_xy"], a["seg_kind"], meta.get("scene_name", "scene"))
+    tri = TriArrays(a["vxy"], a["tri_v"], a["tri_nbr"], a["tri_flag"], scene_name=scene.name)
+    return scene, tri

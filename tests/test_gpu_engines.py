@@ -228,3 +228,39 @@ def test_drop_in_api_on_model_objects():
         accel.locate_triangle(tri, Point(0.5, 0.5), "nope")
     batch = accel.trace_batch(tri, rays_np)
     assert np.array_equal(batch["seg"], ref["seg"])
+
+
+def test_chained_secondary_rays():
+    """mwt_trace_chain_dev: the final triangle of every
+    walk equals the oracle's, and secondary rays started there (no locate)
+    trace identically to the oracle given the same start triangles."""
+    import torch
+    from oracle import oracle as orc
+    from paper_2112_05570_b200.engine import DeviceMesh
+    for cfg in ("lines1024", "hair512"):
+        paths = fixture_paths(cfg, "mwt")
+        m, om = DeviceMesh.from_files(*paths), orc.Mesh.from_files(*paths)
+        rays = orc.raygen(0, box_of(cfg), 7, 0, 1 << 16)
+        ref = om.trace(rays)
+        got = m.trace_chain_device(torch.from_numpy(rays).cuda())
+        got = {k: v.cpu().numpy() for k, v in got.items()}
+        for k in ("end", "seg", "steps"):
+            assert np.array_equal(got[k], ref[k]), (cfg, k)
+        # secondary rays from the hit points, mirrored about the hit segment
+        hit = ref["seg"] >= 0
+        o = rays[hit, :2] + ref["t"][hit, None] * rays[hit, 2:]
+        sc, sid = om.scene, ref["seg"][hit]
+        e = np.stack([sc.bx[sid] - sc.ax[sid], sc.by[sid] - sc.ay[sid]], 1)
+        e /= np.hypot(e[:, 0], e[:, 1])[:, None]
+        d = rays[hit, 2:]
+        d = 2.0 * (d * e).sum(1)[:, None] * e - d  # mirror about the segment
+        d /= np.hypot(d[:, 0], d[:, 1])[:, None]
+        r2 = np.ascontiguousarray(np.concatenate([o, d], 1))
+        start2 = np.ascontiguousarray(ref["end"][hit])
+        ref2 = om.trace(r2, start2)
+        got2 = m.trace_chain_device(torch.from_numpy(r2).cuda(), torch.from_numpy(start2).cuda())
+        got2 = {k: v.cpu().numpy() for k, v in got2.items()}
+        for k in ("end", "seg", "steps"):
+            assert np.array_equal(got2[k], ref2[k]), (cfg, "secondary", k)
+        h2 = ref2["seg"] >= 0
+        assert np.array_equal(got2["t"][h2], ref2["t"][h2])

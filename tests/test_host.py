@@ -140,3 +140,38 @@ def test_shard_ranges():
         assert parts[0].first == 0 and sum(p.count for p in parts) == 1000003
         assert all(parts[k].first + parts[k].count == parts[k + 1].first for k in range(world - 1))
         assert [weak_shard(r, world, 10).first for r in range(world)] == [10 * r for r in range(world)]
+
+
+def test_binary_mesh_roundtrip(tmp_path):
+    """mwt-mesh v1: text -> binary -> identical SoA, and
+    the packer produces the same walk words from either."""
+    import ctypes
+    from paper_2112_05570_b200 import _lib
+    from paper_2112_05570_b200.formats import (FormatError, load_mesh_binary, load_scene, load_tri,
+                                               save_mesh_binary)
+    sp, tp = fixture_paths("lines1024", "mwt")
+    scene, tri = load_scene(sp), load_tri(tp)
+    save_mesh_binary(str(tmp_path / "m"), scene, tri)
+    s2, t2 = load_mesh_binary(str(tmp_path / "m"))
+    assert np.array_equal(s2.xy.view(np.uint64), scene.xy.view(np.uint64))
+    assert np.array_equal(s2.kind, scene.kind)
+    assert np.array_equal(t2.vxy.view(np.uint64), tri.vxy.view(np.uint64))
+    for k in ("v", "nbr", "flag"):
+        assert np.array_equal(getattr(t2, k), getattr(tri, k))
+
+    def words(sc, tr):
+        vxy = np.ascontiguousarray(tr.vxy, np.float64).reshape(-1, 2)
+        vx, vy = np.ascontiguousarray(vxy[:, 0]), np.ascontiguousarray(vxy[:, 1])
+        link = np.empty(4 * len(tr.v), np.int32)
+        P = _lib.ptr
+        i32 = lambda a: np.ascontiguousarray(a, np.int32)  # noqa: E731
+        _lib.check(_lib.lib.mwt_pack_dry_run(
+            P(vx), P(vy), len(vx), P(i32(tr.v)), P(i32(tr.nbr)), P(i32(tr.flag)), len(tr.v),
+            P(np.ascontiguousarray(sc.xy, np.float64)), P(np.ascontiguousarray(sc.kind, np.uint8)),
+            len(sc.kind), P(link), None, None, None), "dry run")
+        return link
+    assert np.array_equal(words(scene, tri), words(s2, t2))
+    (tmp_path / "bad").mkdir()
+    (tmp_path / "bad" / "format.txt").write_text('{"format": "other"}\n')
+    with pytest.raises(FormatError):
+        load_mesh_binary(str(tmp_path / "bad"))
