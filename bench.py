@@ -107,6 +107,18 @@ def fixture(cfg: str, which: str):
     return os.path.join(d, "scene.txt"), os.path.join(d, f"{which}.tri")
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def cpu_reference(cfg: str, which: str, parts, budget_s: float = 20.0, first: int = 0):
     """The reference CPU path (oracle restatement, all host threads) on a
     bounded sample of the workload: returns (rays/s, cores, sample text)."""
@@ -161,7 +173,8 @@ def run_reference_arm(args, rank: int):
         "dtype": "f64", "data": "synthetic (seeded rays, reference-built fixtures)",
         "config": {"workload": f"{args.config}/{args.mesh}",
                    "rays_per_step": {("box_entry" if m == 0 else "interior"): n for m, n in parts}},
-        "cpu_baseline": {"value": v, "unit": "rays/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "rays/s", "cores": cores, "kind": "port", "sample": sample,
+                         "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -329,7 +342,7 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu and not args.profile:
         v, cores, sample = cpu_reference(args.config, args.mesh, parts, budget_s=args.cpu_budget)
         line["cpu_baseline"] = {"value": v, "unit": "rays/s", "cores": cores, "kind": "port",
-                                "sample": sample}
+                                "sample": sample, "cpu_model": cpu_model()}
     if world > 1:
         dist.barrier()
     if rank == 0:
