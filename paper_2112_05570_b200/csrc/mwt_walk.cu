@@ -642,6 +642,7 @@ __device__ __forceinline__ void hist_add_warp(HistSm *H, int seg, int steps, uin
 
 // Epilogue for a lane whose ray has ended (phase 2: exit edge
 // reached; phase 3: TraversalError): hit test, per-ray outputs, histogram.
+template <bool END>
 __device__ __forceinline__ void epilogue(const MeshDev *__restrict__ Mg, const Launch *__restrict__ L,
                                       HistSm *H, long long i, double ox, double oy, double dx,
                                       double dy, int kr, int ch, uint32_t w, double sp, double sq,
@@ -664,7 +665,7 @@ __device__ __forceinline__ void epilogue(const MeshDev *__restrict__ Mg, const L
     if (O.u) O.u[i] = u;
     if (O.steps) O.steps[i] = steps;
     if (O.st) O.st[i] = st;
-    if (O.end) O.end[i] = phase == 2 ? kr / 3 : -1;
+    if (END && O.end) O.end[i] = phase == 2 ? kr / 3 : -1;  // loaded rays only (chaining)
     if (H) hist_add_warp(H, seg, steps, st);
 }
 
@@ -732,7 +733,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         unsigned walking = __ballot_sync(FULL, phase == 1);
         if (__popc(walking) <= refill_below) {
             if (phase >= 2) {
-                epilogue(&M, &L, Hp, idx, r.ox, r.oy, r.dx, r.dy, s.kr, s.ch, s.w, s.sp, s.sq, st,
+                epilogue<!GEN>(&M, &L, Hp, idx, r.ox, r.oy, r.dx, r.dy, s.kr, s.ch, s.w, s.sp, s.sq, st,
                          s.steps, phase);
                 phase = 0;
             }
