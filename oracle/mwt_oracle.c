@@ -143,10 +143,6 @@ static inline uint64_t mix64(uint64_t z) {
 uint64_t orc_ray_key(uint64_t seed, uint64_t stream) {
     return mix64(mix64(seed + GOLDEN) ^ (stream * 0xD1B54A32D192ED03ull));
 }
-static inline double u01(uint64_t s0, uint64_t k) {
-    return (double)(mix64(s0 + (k + 1) * GOLDEN) >> 11) * 0x1p-53;
-}
-
 /* mode 0: box-entry isotropic line rays; mode 1: interior origins */
 void orc_raygen_one(int mode, const double box[4], uint64_t key, uint64_t idx, double out[4]) {
     uint64_t s0 = key ^ idx; /* per-ray SplitMix64 stream: mix64(s0 + (k + 1) * golden) */
@@ -168,7 +164,8 @@ void orc_raygen_one(int mode, const double box[4], uint64_t key, uint64_t idx, d
     }
     double x0 = box[0], y0 = box[1], x1 = box[2], y1 = box[3];
     double W = x1 - x0, H = y1 - y0;
-    double u = u01(s0, 128), v = u01(s0, 129);
+    uint64_t zuv = mix64(s0 + 129 * GOLDEN); /* draw 128: u, v = its 32-bit halves * 2^-32 */
+    double u = (double)(uint32_t)(zuv >> 32) * 0x1p-32, v = (double)(uint32_t)zuv * 0x1p-32;
     double ox, oy;
     if (mode == 1) {
         ox = x0 + W * u;

@@ -3,8 +3,9 @@
 TEST INFRASTRUCTURE ONLY (see oracle/mwt_oracle.c header).  Bit-identical to
 ``orc_raygen`` (oracle/mwt_oracle.c) and to the device generator in
 ``paper_2112_05570_b200/csrc/mwt_kernels.cu``: counter-based SplitMix64 draws
-keyed by (seed, stream, ray index), doubles from the top 53 bits, isotropic
-directions by unit-disk rejection + IEEE sqrt and division (no cos/sin), and
+keyed by (seed, stream, ray index); isotropic directions by unit-disk rejection
+on 32-bit coordinates and angle doubling (one IEEE division, no cos/sin/sqrt);
+the side / offset draws are the two 32-bit halves of one draw; and
 only + - * / sqrt afterwards (numpy never fuses a*b+c).
 
 The reference has no box-entry generator; its ``sample_rays``
@@ -39,12 +40,6 @@ def ray_key(seed: int, stream: int) -> np.uint64:
         return _mix(a ^ (np.uint64(stream) * STREAM_MUL))
 
 
-def _u01(s0, k: int):
-    with np.errstate(over="ignore"):
-        z = _mix(s0 + np.uint64(k + 1) * GOLDEN)
-    return (z >> np.uint64(11)).astype(np.float64) * (2.0 ** -53)
-
-
 def raygen(mode: int, box, seed: int, first: int, n: int) -> np.ndarray:
     """(n, 4) float64 array of rays (ox, oy, dx, dy)."""
     key = ray_key(seed, mode)
@@ -76,7 +71,10 @@ def raygen(mode: int, box, seed: int, first: int, n: int) -> np.ndarray:
     dy = np.where(ok, (2.0 * x * y) * inv, 0.0)
     x0, y0, x1, y1 = (float(v) for v in box)
     W, H = x1 - x0, y1 - y0
-    u, v = _u01(s0, 128), _u01(s0, 129)
+    with np.errstate(over="ignore"):
+        zuv = _mix(s0 + np.uint64(129) * GOLDEN)  # draw 128: u, v = its 32-bit halves * 2^-32
+    u = (zuv >> np.uint64(32)).astype(np.float64) * 2.0 ** -32
+    v = (zuv & np.uint64(0xFFFFFFFF)).astype(np.float64) * 2.0 ** -32
     if mode == MODE_INTERIOR:
         ox = x0 + W * u
         oy = y0 + H * v

@@ -159,11 +159,6 @@ static inline unsigned long long ray_key(unsigned long long seed, unsigned long 
     return mix64(mix64(seed + kGolden) ^ (stream * 0xD1B54A32D192ED03ull));
 }
 
-// draw k of ray state s0: 53-bit uniform in [0, 1)
-__device__ __forceinline__ double u01(unsigned long long s0, unsigned long long k) {
-    return (double)(mix64(s0 + (k + 1ull) * kGolden) >> 11) * 0x1p-53;
-}
-
 // rejection attempt a: one 64-bit draw -> two 32-bit coordinates in [-1, 1)
 __device__ __forceinline__ void disk_try(unsigned long long s0, int a, double &x, double &y,
                                          double &r2) {
@@ -213,7 +208,12 @@ __device__ __forceinline__ Ray gen_ray(int mode, const Box &b, unsigned long lon
         r.dy = ok ? (2.0 * x * y) * inv : 0.0;
     }
     const double W = b.x1 - b.x0, H = b.y1 - b.y0;
-    const double u = u01(s0, 128), v = u01(s0, 129);
+    // u, v: the two 32-bit halves of draw 128 (hi * 2^-32, lo * 2^-32), built
+    // as 1 + h * 2^-32 - 1 (exact)
+    const unsigned long long zuv = mix64(s0 + 129ull * kGolden);
+    const unsigned uh = (unsigned)(zuv >> 32), vl = (unsigned)zuv;
+    const double u = __hiloint2double((int)(0x3FF00000u | (uh >> 12)), (int)(uh << 20)) - 1.0;
+    const double v = __hiloint2double((int)(0x3FF00000u | (vl >> 12)), (int)(vl << 20)) - 1.0;
     if (mode == MWT_RAYS_INTERIOR) {
         r.ox = b.x0 + W * u;
         r.oy = b.y0 + H * v;
