@@ -125,6 +125,7 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
                    Arena::align(P.bu.size() * 8) + Arena::align(P.bpq.size() * 8) +
                    Arena::align(P.bword.size() * 4) + Arena::align(P.bbucket.size() * 4) +
                    Arena::align(P.crec.size() * 4) +
+                   Arena::align((P.bu.size() + P.bpq.size()) * 8 + P.bword.size() * 4 + P.bbucket.size() * 4 + 64) +
                    Arena::align(P.vxy.size() * 8);
     Arena a;
     CK(cudaMalloc(&a.base, bytes));
@@ -147,6 +148,17 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     int32_t *bbucket = carve<int32_t>(a, P.bbucket.size());
     uint32_t *crec = carve<uint32_t>(a, P.crec.size());
     double *vxy = carve<double>(a, P.vxy.size());
+    // boundary blob: bu | bpq | bword | bbucket, each 16-B aligned
+    auto a16 = [](size_t b) { return (b + 15) & ~(size_t)15; };
+    const size_t bo_bpq = a16(P.bu.size() * 8), bo_bword = bo_bpq + a16(P.bpq.size() * 8),
+                 bo_bbucket = bo_bword + a16(P.bword.size() * 4),
+                 bblob_bytes = bo_bbucket + a16(P.bbucket.size() * 4);
+    std::vector<unsigned char> bblob_host(bblob_bytes, 0);
+    std::memcpy(bblob_host.data(), P.bu.data(), P.bu.size() * 8);
+    std::memcpy(bblob_host.data() + bo_bpq, P.bpq.data(), P.bpq.size() * 8);
+    std::memcpy(bblob_host.data() + bo_bword, P.bword.data(), P.bword.size() * 4);
+    std::memcpy(bblob_host.data() + bo_bbucket, P.bbucket.data(), P.bbucket.size() * 4);
+    unsigned char *bblob = carve<unsigned char>(a, bblob_bytes);
     cudaError_t e = cudaSuccess;
     auto up = [&](void *dst, const void *src, size_t n) {
         if (e == cudaSuccess && n) e = cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
@@ -166,6 +178,7 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     up(bbucket, P.bbucket.data(), P.bbucket.size() * 4);
     up(crec, P.crec.data(), P.crec.size() * 4);
     up(vxy, P.vxy.data(), P.vxy.size() * 8);
+    up(bblob, bblob_host.data(), bblob_bytes);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) {
         cudaFree(a.base);
@@ -184,12 +197,17 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     m->dev.bpq = reinterpret_cast<const double4 *>(bpq);
     m->dev.bword = bword;
     m->dev.bbucket = bbucket;
+    m->dev.bblob = reinterpret_cast<const uint4 *>(bblob);
+    m->dev.bblob_bytes = (int32_t)bblob_bytes;
+    m->dev.bo_bpq = (int32_t)bo_bpq;
+    m->dev.bo_bword = (int32_t)bo_bword;
+    m->dev.bo_bbucket = (int32_t)bo_bbucket;
     if (!P.crec.empty()) {
         m->dev.crec = reinterpret_cast<const uint2 *>(crec);
         m->dev.vxy = reinterpret_cast<const double2 *>(vxy);
         m->dev.crec_bytes = (int32_t)(P.crec.size() * 4);
         const int64_t sm = (int64_t)m->dev.crec_bytes + 16LL * P.nv;
-        m->dev.smem_bytes = sm <= mwt::kSmemWalkMax ? (int32_t)sm : 0;
+        m->dev.smem_bytes = sm + (int64_t)bblob_bytes <= mwt::kSmemWalkMax ? (int32_t)sm : 0;
     }
     m->info.num_vertices = P.nv;
     m->info.num_triangles = P.nt;

@@ -131,6 +131,10 @@ struct MeshDev {
     const double2 *vxy;
     int32_t crec_bytes;  // 16-B padded size of crec; vxy follows it in shared memory
     int32_t smem_bytes;  // crec_bytes + 16 * nv if the table fits kSmemWalkMax, else 0
+    // the boundary-edge table as one blob (staged next to the walk table):
+    // bu at 0, bpq at bo_bpq, bword at bo_bword, bbucket at bo_bbucket (bytes)
+    const uint4 *bblob;
+    int32_t bblob_bytes, bo_bpq, bo_bword, bo_bbucket;
 };
 
 struct BvhDev {

@@ -497,7 +497,14 @@ struct Init {
 // (side(Q) < 0 < side(P)) the first-triangle scan of accel.py:171-191 reduces
 // to an ordinary step entered through that edge: it is no candidate (sp > 0)
 // and has trans < 0, so neither the exit nor the fallback choice can pick it.
-__device__ __forceinline__ bool boundary_start(const MeshDev &M, const Ray &r, WalkState &s) {
+struct BTab {  // the boundary-edge table arrays (global or a shared-memory copy)
+    const double2 *bu;
+    const double4 *bpq;
+    const int32_t *bword, *bbucket;
+};
+
+__device__ __forceinline__ bool boundary_start(const MeshDev &M, const BTab &T, const Ray &r,
+                                               WalkState &s) {
     if (!(M.flood_filter && fabs(r.ox) <= 4.0 && fabs(r.oy) <= 4.0)) return false;
     int k0 = 0, k1 = M.nbsides;
     if (M.unit_sides) {  // bottom, right, top, left
@@ -512,12 +519,12 @@ __device__ __forceinline__ bool boundary_start(const MeshDev &M, const Ray &r, W
         if (!(u > S.lo && u < S.hi)) return false;
         int b = (int)((u - S.lo) * S.scale);
         b = b < 0 ? 0 : (b >= S.nb ? S.nb - 1 : b);
-        int e = __ldg(M.bbucket + S.boff + b);
-        double2 U = __ldg(M.bu + S.off + e);
-        while (u >= U.y && e < S.cnt - 1) U = __ldg(M.bu + S.off + (++e));
+        int e = T.bbucket[S.boff + b];
+        double2 U = T.bu[S.off + e];
+        while (u >= U.y && e < S.cnt - 1) U = T.bu[S.off + (++e)];
         if (!(U.x < u && u < U.y)) return false;  // on a vertex: general path
-        const double4 PQ = ldg4d(M.bpq + S.off + e);
-        const uint32_t word = (uint32_t)__ldg(M.bword + S.off + e);
+        const double4 PQ = T.bpq[S.off + e];
+        const uint32_t word = (uint32_t)T.bword[S.off + e];
         const double2 P = make_double2(PQ.x, PQ.y), Q = make_double2(PQ.z, PQ.w);
         const double2 A = __ldg(M.cxy + word);  // apex corner j of T: cxy[3T + j], word = 3T + j
         // _contains values in the reference's form: edge i -> (corner i+1, corner i+2)
@@ -540,7 +547,8 @@ __device__ __forceinline__ bool boundary_start(const MeshDev &M, const Ray &r, W
 }
 
 template <bool GEN>
-__device__ __forceinline__ Init prologue_body(const MeshDev &M, const RaySrc &src, long long i) {
+__device__ __forceinline__ Init prologue_body(const MeshDev &M, const BTab &T, const RaySrc &src,
+                                              long long i) {
     Init o;
     o.st = 0;
     const Ray r = GEN ? gen_ray(src.mode, src.box, src.key, src.first + (unsigned long long)i)
@@ -548,7 +556,7 @@ __device__ __forceinline__ Init prologue_body(const MeshDev &M, const RaySrc &sr
     o.ox = r.ox; o.oy = r.oy; o.dx = r.dx; o.dy = r.dy;
     if (!src.start) {
         WalkState bs;
-        if (boundary_start(M, r, bs)) {
+        if (boundary_start(M, T, r, bs)) {
             o.start = bs.kr / 3;
             o.sp = bs.sp; o.sq = bs.sq; o.w = bs.w; o.cur = bs.kr; o.ei = bs.ch; o.steps = 0;
             o.fast = true;
@@ -601,8 +609,8 @@ struct InitP {
 
 template <bool GEN>
 __device__ __forceinline__ InitP prologue(long long i, const Launch *__restrict__ L,
-                                       const MeshDev *__restrict__ Mg) {
-    const Init in = prologue_body<GEN>(*Mg, L->src, i);
+                                       const MeshDev *__restrict__ Mg, const BTab &T) {
+    const Init in = prologue_body<GEN>(*Mg, T, L->src, i);
     if (L->out.start) L->out.start[i] = in.start;
     InitP o;
     o.ox = in.ox; o.oy = in.oy; o.dx = in.dx; o.dy = in.dy; o.sp = in.sp; o.sq = in.sq;
@@ -695,12 +703,19 @@ __global__ void __launch_bounds__(THREADS, MINB)
     extern __shared__ __align__(16) unsigned char dsm[];
     const uint2 *srec = reinterpret_cast<const uint2 *>(dsm);
     const double2 *svxy = reinterpret_cast<const double2 *>(dsm + (SMEM ? M.crec_bytes : 0));
+    BTab btab{M.bu, M.bpq, M.bword, M.bbucket};
     if (SMEM) {
-        const int n16 = M.smem_bytes >> 4, c16 = M.crec_bytes >> 4;
+        const int n16 = M.smem_bytes >> 4, c16 = M.crec_bytes >> 4, b16 = M.bblob_bytes >> 4;
         uint4 *d = reinterpret_cast<uint4 *>(dsm);
         const uint4 *a = reinterpret_cast<const uint4 *>(M.crec);
         const uint4 *b = reinterpret_cast<const uint4 *>(M.vxy);
         for (int k = threadIdx.x; k < n16; k += THREADS) d[k] = k < c16 ? __ldg(a + k) : __ldg(b + (k - c16));
+        for (int k = threadIdx.x; k < b16; k += THREADS) d[n16 + k] = __ldg(M.bblob + k);
+        const unsigned char *bb = dsm + M.smem_bytes;
+        btab.bu = reinterpret_cast<const double2 *>(bb);
+        btab.bpq = reinterpret_cast<const double4 *>(bb + M.bo_bpq);
+        btab.bword = reinterpret_cast<const int32_t *>(bb + M.bo_bword);
+        btab.bbucket = reinterpret_cast<const int32_t *>(bb + M.bo_bbucket);
     }
     const long long per = (n + gridDim.x - 1) / gridDim.x;
     const long long cbeg = (long long)blockIdx.x * per;
@@ -755,7 +770,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     const long long i = rank < rem ? next + rank : nb + (rank - rem);
                     if (rank < rem || i < ne) {
                         idx = i;
-                        const InitP in = prologue<GEN>(i, &L, &M);
+                        const InitP in = prologue<GEN>(i, &L, &M, btab);
                         r.ox = in.ox; r.oy = in.oy; r.dx = in.dx; r.dy = in.dy;
                         s.sp = in.sp; s.sq = in.sq; s.w = in.w; s.kr = in.kr;
                         st = in.st;
@@ -924,9 +939,9 @@ template <bool GEN, int MINB, int THREADS, bool SMEM>
 static bool launch_k_trace(const MeshDev &m, const Launch &L, long long n, long long *hist,
                            void *stream) {
     auto kern = k_trace<GEN, MINB, THREADS, SMEM>;
-    const int dyn = SMEM ? m.smem_bytes : 0;
+    const int dyn = SMEM ? m.smem_bytes + m.bblob_bytes : 0;
     if (SMEM) {
-        if (dyn <= 0) return false;
+        if (m.smem_bytes <= 0) return false;  // the walk table does not fit: variant 1
         int dev = 0;
         cudaGetDevice(&dev);
         static bool attr_set[2][64] = {};
