@@ -208,6 +208,8 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
         m->dev.crec_bytes = (int32_t)(P.crec.size() * 4);
         const int64_t sm = (int64_t)m->dev.crec_bytes + 16LL * P.nv;
         m->dev.smem_bytes = sm + (int64_t)bblob_bytes <= mwt::kSmemWalkMax ? (int32_t)sm : 0;
+        m->dev.seg_staged = m->dev.smem_bytes > 0 &&
+                            sm + (int64_t)bblob_bytes + 32LL * P.ns <= mwt::kSmemWalkMax;
     }
     m->info.num_vertices = P.nv;
     m->info.num_triangles = P.nt;

@@ -135,6 +135,7 @@ struct MeshDev {
     // bu at 0, bpq at bo_bpq, bword at bo_bword, bbucket at bo_bbucket (bytes)
     const uint4 *bblob;
     int32_t bblob_bytes, bo_bpq, bo_bword, bo_bbucket;
+    int32_t seg_staged;  // the segments (32 B each) also fit: staged after the blob
 };
 
 struct BvhDev {

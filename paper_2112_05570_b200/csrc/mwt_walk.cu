@@ -366,13 +366,15 @@ __device__ __forceinline__ bool walk_step(const MeshDev &M, const Ray &r, WalkSt
 }
 
 // constrained / open exit: accel.py:192-211
+// (sseg: a shared-memory copy of the segments, or NULL)
 __device__ __forceinline__ int walk_terminal(const MeshDev &M, const Ray &r, const WalkState &s,
-                                          double &ot, double &ou, uint32_t &st) {
+                                          double &ot, double &ou, uint32_t &st,
+                                          const double4 *sseg = nullptr) {
     ot = CUDART_NAN;
     ou = CUDART_NAN;
     if (s.w == kOpenWord || (s.w & kBoundaryBit)) return -1;
     const int sid = (int)(s.w & kSidMask);
-    const double4 S = ldg4d(M.seg + sid);
+    const double4 S = sseg ? sseg[sid] : ldg4d(M.seg + sid);
     double t, u;
     bool par = false;
     bool ok = rsi(r, S, t, u, par);
@@ -652,7 +654,7 @@ __device__ __forceinline__ void hist_add_warp(HistSm *H, int seg, int steps, uin
 // reached; phase 3: TraversalError): hit test, per-ray outputs, histogram.
 template <bool END>
 __device__ __forceinline__ void epilogue(const MeshDev *__restrict__ Mg, const Launch *__restrict__ L,
-                                      HistSm *H, long long i, double ox, double oy, double dx,
+                                      HistSm *H, const double4 *sseg, long long i, double ox, double oy, double dx,
                                       double dy, int kr, int ch, uint32_t w, double sp, double sq,
                                       uint32_t st, int steps, int phase) {
     int seg = -1;
@@ -665,7 +667,7 @@ __device__ __forceinline__ void epilogue(const MeshDev *__restrict__ Mg, const L
         s.w = w;
         s.sp = sp;
         s.sq = sq;
-        seg = walk_terminal(*Mg, r, s, t, u, st);
+        seg = walk_terminal(*Mg, r, s, t, u, st, sseg);
     }
     const TraceOut &O = L->out;
     if (O.seg) O.seg[i] = seg;
@@ -704,6 +706,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const uint2 *srec = reinterpret_cast<const uint2 *>(dsm);
     const double2 *svxy = reinterpret_cast<const double2 *>(dsm + (SMEM ? M.crec_bytes : 0));
     BTab btab{M.bu, M.bpq, M.bword, M.bbucket};
+    const double4 *sseg = nullptr;
     if (SMEM) {
         const int n16 = M.smem_bytes >> 4, c16 = M.crec_bytes >> 4, b16 = M.bblob_bytes >> 4;
         uint4 *d = reinterpret_cast<uint4 *>(dsm);
@@ -716,6 +719,12 @@ __global__ void __launch_bounds__(THREADS, MINB)
         btab.bpq = reinterpret_cast<const double4 *>(bb + M.bo_bpq);
         btab.bword = reinterpret_cast<const int32_t *>(bb + M.bo_bword);
         btab.bbucket = reinterpret_cast<const int32_t *>(bb + M.bo_bbucket);
+        if (M.seg_staged) {
+            uint4 *ds = reinterpret_cast<uint4 *>(dsm + M.smem_bytes + M.bblob_bytes);
+            const uint4 *gs = reinterpret_cast<const uint4 *>(M.seg);
+            for (int k = threadIdx.x; k < 2 * M.ns; k += THREADS) ds[k] = __ldg(gs + k);
+            sseg = reinterpret_cast<const double4 *>(ds);
+        }
     }
     const long long per = (n + gridDim.x - 1) / gridDim.x;
     const long long cbeg = (long long)blockIdx.x * per;
@@ -748,7 +757,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         unsigned walking = __ballot_sync(FULL, phase == 1);
         if (__popc(walking) <= refill_below) {
             if (phase >= 2) {
-                epilogue<!GEN>(&M, &L, Hp, idx, r.ox, r.oy, r.dx, r.dy, s.kr, s.ch, s.w, s.sp, s.sq, st,
+                epilogue<!GEN>(&M, &L, Hp, sseg, idx, r.ox, r.oy, r.dx, r.dy, s.kr, s.ch, s.w, s.sp, s.sq, st,
                          s.steps, phase);
                 phase = 0;
             }
@@ -939,7 +948,7 @@ template <bool GEN, int MINB, int THREADS, bool SMEM>
 static bool launch_k_trace(const MeshDev &m, const Launch &L, long long n, long long *hist,
                            void *stream) {
     auto kern = k_trace<GEN, MINB, THREADS, SMEM>;
-    const int dyn = SMEM ? m.smem_bytes + m.bblob_bytes : 0;
+    const int dyn = SMEM ? m.smem_bytes + m.bblob_bytes + (m.seg_staged ? 32 * m.ns : 0) : 0;
     if (SMEM) {
         if (m.smem_bytes <= 0) return false;  // the walk table does not fit: variant 1
         int dev = 0;
