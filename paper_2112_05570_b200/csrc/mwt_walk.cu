@@ -621,8 +621,8 @@ __device__ __forceinline__ InitP prologue(long long i, const Launch *__restrict_
     return o;
 }
 
-// Block-private histogram with warp-aggregated updates: one shared atomic per
-// distinct step bin in the warp, one per hit / miss / status bit present.
+// Block-private histogram: a shared atomic per lane for its step bin,
+// warp-aggregated updates for hit / miss / the step sum / each status bit present.
 struct HistSm {
     unsigned int bins[MWT_HIST_LEN];
     unsigned long long steps_sum;
@@ -632,8 +632,7 @@ __device__ __forceinline__ void hist_add_warp(HistSm *H, int seg, int steps, uin
     const unsigned m = __activemask();
     const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
     const int bin = steps < MWT_HIST_STEP_BINS - 1 ? (steps < 0 ? 0 : steps) : MWT_HIST_STEP_BINS - 1;
-    const unsigned same = __match_any_sync(m, bin);
-    if (lane == __ffs(same) - 1) atomicAdd(H->bins + bin, (unsigned)__popc(same));
+    atomicAdd(H->bins + bin, 1u);  // per lane: cheaper than grouping equal bins (match.any)
     const unsigned hits = __ballot_sync(m, seg >= 0);
     const unsigned ssum = __reduce_add_sync(m, (unsigned)(steps > 0 ? steps : 0));
     unsigned any = __reduce_or_sync(m, st) & 0xFFFu;
