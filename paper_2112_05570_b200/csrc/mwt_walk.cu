@@ -952,13 +952,15 @@ static bool launch_k_trace(const MeshDev &m, const Launch &L, long long n, long 
         if (m.smem_bytes <= 0) return false;  // the walk table does not fit: variant 1
         int dev = 0;
         cudaGetDevice(&dev);
-        static bool attr_set[2][64] = {};
         if (dev < 0 || dev >= 64) return false;
-        if (!attr_set[GEN][dev]) {
-            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmemWalkMax) !=
-                cudaSuccess)
+        static int attr_set[64] = {};  // per instantiation and device: enabled dynamic size
+        if (attr_set[dev] < dyn) {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) !=
+                cudaSuccess) {
+                (void)cudaGetLastError();  // does not fit: the caller falls back
                 return false;
-            attr_set[GEN][dev] = true;
+            }
+            attr_set[dev] = dyn;
         }
     }
     kern<<<persistent_grid(kern, n, THREADS, dyn), THREADS, dyn, (cudaStream_t)stream>>>(
