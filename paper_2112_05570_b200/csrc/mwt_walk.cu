@@ -34,6 +34,19 @@ __device__ __forceinline__ void corners(const MeshDev &M, int t, double2 &P0, do
     P2 = __ldg(M.cxy + 3 * t + 2);
 }
 
+// corners from the shared-memory walk table when staged (record 3t+k holds
+// the vertex id of corner k), else from cxy
+__device__ __forceinline__ void corners2(const MeshDev &M, const uint2 *srec, const double2 *svxy,
+                                         int t, double2 &P0, double2 &P1, double2 &P2) {
+    if (srec) {
+        P0 = svxy[srec[3 * t].x >> kCVidShift];
+        P1 = svxy[srec[3 * t + 1].x >> kCVidShift];
+        P2 = svxy[srec[3 * t + 2].x >> kCVidShift];
+    } else {
+        corners(M, t, P0, P1, P2);
+    }
+}
+
 // accel.py:219-223 with geometry.py:81-83 per edge i: signed_area2(P[i+1], P[i+2], p)
 __device__ __forceinline__ void edge_areas(double2 P0, double2 P1, double2 P2, double px, double py,
                                            double &e0, double &e1, double &e2) {
@@ -129,7 +142,8 @@ __device__ __noinline__ LocRes flood(const double2 *cxy, const int4 *lnbr, int f
 
 // returns the start triangle and its corners
 __device__ __forceinline__ int locate(const MeshDev &M, double px, double py, uint32_t &st,
-                                      double2 &P0, double2 &P1, double2 &P2) {
+                                      double2 &P0, double2 &P1, double2 &P2,
+                                      const uint2 *srec = nullptr, const double2 *svxy = nullptr) {
     const int res = M.res;
     const double dres = (double)res;
     double vx = px * dres, vy = py * dres;
@@ -142,7 +156,7 @@ __device__ __forceinline__ int locate(const MeshDev &M, double px, double py, ui
     const double dx = px - sx, dy = py - sy;
     int cur = __ldg(M.anchor + cy * res + cx);
     double e0, e1, e2;
-    corners(M, cur, P0, P1, P2);
+    corners2(M, srec, svxy, cur, P0, P1, P2);
     edge_areas(P0, P1, P2, px, py, e0, e1, e2);
     if (!inside(e0, e1, e2)) {  // seed cell centre and p in different triangles
         int ent = -1;
@@ -163,7 +177,7 @@ __device__ __forceinline__ int locate(const MeshDev &M, double px, double py, ui
             if (word < 0) break;
             cur = word >> 2;
             ent = word & 3;
-            corners(M, cur, P0, P1, P2);
+            corners2(M, srec, svxy, cur, P0, P1, P2);
             edge_areas(P0, P1, P2, px, py, e0, e1, e2);
             if (inside(e0, e1, e2)) {
                 found = true;
@@ -174,7 +188,7 @@ __device__ __forceinline__ int locate(const MeshDev &M, double px, double py, ui
             const LocRes lr = loc_brute(M.cxy, M.nt, px, py);
             st |= ST_LOC_BRUTE | lr.st;
             cur = lr.tid;
-            corners(M, cur, P0, P1, P2);
+            corners2(M, srec, svxy, cur, P0, P1, P2);
             edge_areas(P0, P1, P2, px, py, e0, e1, e2);
         }
     }
@@ -189,7 +203,7 @@ __device__ __forceinline__ int locate(const MeshDev &M, double px, double py, ui
     const LocRes fr = flood(M.cxy, M.lnbr, M.flood_filter, cur, px, py);
     st |= fr.st;
     const int best = fr.tid;
-    if (best != cur) corners(M, best, P0, P1, P2);
+    if (best != cur) corners2(M, srec, svxy, best, P0, P1, P2);
     return best;
 }
 
@@ -503,6 +517,8 @@ struct BTab {  // the boundary-edge table arrays (global or a shared-memory copy
     const double2 *bu;
     const double4 *bpq;
     const int32_t *bword, *bbucket;
+    const uint2 *srec;  // the staged walk table (corners for locate), or NULL
+    const double2 *svxy;
 };
 
 __device__ __forceinline__ bool boundary_start(const MeshDev &M, const BTab &T, const Ray &r,
@@ -574,7 +590,7 @@ __device__ __forceinline__ Init prologue_body(const MeshDev &M, const BTab &T, c
         if (t0 < 0 || t0 >= M.nt) t0 = -1;
         else corners(M, t0, P0, P1, P2);
     } else {
-        t0 = locate(M, r.ox, r.oy, o.st, P0, P1, P2);
+        t0 = locate(M, r.ox, r.oy, o.st, P0, P1, P2, T.srec, T.svxy);
     }
     o.start = t0;
     WalkState s;
@@ -704,7 +720,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     extern __shared__ __align__(16) unsigned char dsm[];
     const uint2 *srec = reinterpret_cast<const uint2 *>(dsm);
     const double2 *svxy = reinterpret_cast<const double2 *>(dsm + (SMEM ? M.crec_bytes : 0));
-    BTab btab{M.bu, M.bpq, M.bword, M.bbucket};
+    BTab btab{M.bu, M.bpq, M.bword, M.bbucket, nullptr, nullptr};
     const double4 *sseg = nullptr;
     if (SMEM) {
         const int n16 = M.smem_bytes >> 4, c16 = M.crec_bytes >> 4, b16 = M.bblob_bytes >> 4;
@@ -718,6 +734,8 @@ __global__ void __launch_bounds__(THREADS, MINB)
         btab.bpq = reinterpret_cast<const double4 *>(bb + M.bo_bpq);
         btab.bword = reinterpret_cast<const int32_t *>(bb + M.bo_bword);
         btab.bbucket = reinterpret_cast<const int32_t *>(bb + M.bo_bbucket);
+        btab.srec = srec;
+        btab.svxy = svxy;
         if (M.seg_staged) {
             uint4 *ds = reinterpret_cast<uint4 *>(dsm + M.smem_bytes + M.bblob_bytes);
             const uint4 *gs = reinterpret_cast<const uint4 *>(M.seg);
