@@ -34,6 +34,12 @@ __device__ __forceinline__ void corners(const MeshDev &M, int t, double2 &P0, do
     P2 = __ldg(M.cxy + 3 * t + 2);
 }
 
+// compact stop word (shared-memory table) -> full walk word
+__device__ __forceinline__ uint32_t expand_cword(uint32_t c) {
+    if (c == kCOpen) return kOpenWord;
+    return kStopBit | ((c & kCBoundary) ? kBoundaryBit : 0u) | (c & 0xFFFFu);
+}
+
 // corners from the shared-memory walk table when staged (record 3t+k holds
 // the vertex id of corner k), else from cxy
 __device__ __forceinline__ void corners2(const MeshDev &M, const uint2 *srec, const double2 *svxy,
@@ -564,6 +570,17 @@ __device__ __forceinline__ bool boundary_start(const MeshDev &M, const BTab &T, 
     return false;
 }
 
+// the walk words of triangle t's three edges: from the staged walk table when
+// present (record 3t+2 holds edges 0 and 1, record 3t holds edge 2), else link[t]
+__device__ __forceinline__ int4 link_words(const MeshDev &M, const BTab &T, int t) {
+    if (!T.srec) return __ldg(M.link + t);
+    const uint2 a = T.srec[3 * t + 2], b = T.srec[3 * t];
+    const uint32_t w0 = a.x & kCWordMask, w1 = a.y, w2 = b.y;
+    return make_int4((int)((w0 & kCStop) ? expand_cword(w0) : w0),
+                     (int)((w1 & kCStop) ? expand_cword(w1) : w1),
+                     (int)((w2 & kCStop) ? expand_cword(w2) : w2), 0);
+}
+
 template <bool GEN>
 __device__ __forceinline__ Init prologue_body(const MeshDev &M, const BTab &T, const RaySrc &src,
                                               long long i) {
@@ -604,7 +621,7 @@ __device__ __forceinline__ Init prologue_body(const MeshDev &M, const BTab &T, c
         o.st |= ST_ERROR;
         s.steps = 0;
         o.phase = 3;
-    } else if (!walk_first(r, t0, __ldg(M.link + t0), P0, P1, P2, s, o.st)) {
+    } else if (!walk_first(r, t0, link_words(M, T, t0), P0, P1, P2, s, o.st)) {
         o.phase = 3;
     } else {
         o.phase = (s.w & kStopBit) ? 2 : 1;
@@ -694,11 +711,6 @@ __device__ __forceinline__ void epilogue(const MeshDev *__restrict__ Mg, const L
     if (H) hist_add_warp(H, seg, steps, st);
 }
 
-// compact stop word (shared-memory table) -> full walk word
-__device__ __forceinline__ uint32_t expand_cword(uint32_t c) {
-    if (c == kCOpen) return kOpenWord;
-    return kStopBit | ((c & kCBoundary) ? kBoundaryBit : 0u) | (c & 0xFFFFu);
-}
 
 constexpr int kGrab = 128;  // rays a warp takes from its CTA's counter at a time
 
