@@ -843,35 +843,34 @@ __global__ void __launch_bounds__(THREADS, MINB)
             while (__popc(__ballot_sync(FULL, fl)) > thr) {
 #pragma unroll
                 for (int u2 = 0; u2 < 4; u2++) {
-                    if (fl) {
-                        const uint32_t k = s.w;
-                        uint32_t wx, wy;
-                        double2 A;
-                        if (SMEM) {
-                            const uint2 X = srec[k];
-                            A = svxy[X.x >> kCVidShift];
-                            wx = X.x & kCWordMask;
-                            wy = X.y;
-                        } else {
-                            int4 W;
-                            load_step_issue(M, k, W, A);
-                            wx = (uint32_t)W.x;
-                            wy = (uint32_t)W.y;
-                        }
-                        const double c = side_of(r, A);
-                        // branch-free commit (c == 0: nothing changes, the lane leaves)
-                        const bool ok = c != 0.0, pos = c > 0.0;
-                        const uint32_t nw = pos ? wx : wy;
-                        s.steps += ok ? 1 : 0;
-                        s.kr = ok ? (int)k : s.kr;
-                        s.sq = pos ? c : s.sq;
-                        s.sp = (ok && !pos) ? c : s.sp;
-                        s.ch = ok ? (pos ? 0 : 1) : s.ch;
-                        s.w = ok ? nw : s.w;
-                        const bool stop = ok && (nw & (SMEM ? kCStop : kStopBit));
-                        phase = stop ? 2 : phase;
-                        fl = ok && !stop && s.steps < lim;
+                    // predicated, not branched: lanes that left compute on record 0
+                    // and commit nothing
+                    const uint32_t k = fl ? s.w : 0u;
+                    uint32_t wx, wy;
+                    double2 A;
+                    if (SMEM) {
+                        const uint2 X = srec[k];
+                        A = svxy[X.x >> kCVidShift];
+                        wx = X.x & kCWordMask;
+                        wy = X.y;
+                    } else {
+                        int4 W;
+                        load_step_issue(M, k, W, A);
+                        wx = (uint32_t)W.x;
+                        wy = (uint32_t)W.y;
                     }
+                    const double c = side_of(r, A);
+                    const bool ok = fl && c != 0.0, pos = c > 0.0;
+                    const uint32_t nw = pos ? wx : wy;
+                    s.steps += ok ? 1 : 0;
+                    s.kr = ok ? (int)k : s.kr;
+                    s.sq = (ok && pos) ? c : s.sq;
+                    s.sp = (ok && !pos) ? c : s.sp;
+                    s.ch = ok ? (pos ? 0 : 1) : s.ch;
+                    s.w = ok ? nw : s.w;
+                    const bool stop = ok && (nw & (SMEM ? kCStop : kStopBit));
+                    phase = stop ? 2 : phase;
+                    fl = ok && !stop && s.steps < lim;
                 }
             }
         }
