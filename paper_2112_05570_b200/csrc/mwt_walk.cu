@@ -529,35 +529,37 @@ struct BTab {  // the boundary-edge table arrays (global or a shared-memory copy
 
 __device__ __forceinline__ bool boundary_start(const MeshDev &M, const BTab &T, const Ray &r,
                                                WalkState &s) {
-    if (!(M.flood_filter && fabs(r.ox) <= 4.0 && fabs(r.oy) <= 4.0)) return false;
-    int k0 = 0, k1 = M.nbsides;
+    // one validity flag instead of early returns (fewer divergent branches);
+    // indices stay in range when a condition fails
+    bool ok = M.flood_filter && fabs(r.ox) <= 4.0 && fabs(r.oy) <= 4.0;
+    int k = -1;
     if (M.unit_sides) {  // bottom, right, top, left
-        k0 = r.oy == 0.0 ? 0 : (r.ox == 1.0 ? 1 : (r.oy == 1.0 ? 2 : (r.ox == 0.0 ? 3 : -1)));
-        if (k0 < 0) return false;
-        k1 = k0 + 1;
+        k = r.oy == 0.0 ? 0 : (r.ox == 1.0 ? 1 : (r.oy == 1.0 ? 2 : (r.ox == 0.0 ? 3 : -1)));
+    } else {
+        for (int kk = M.nbsides - 1; kk >= 0; kk--)
+            if ((M.bs[kk].axis == 0 ? r.oy : r.ox) == M.bs[kk].c) k = kk;
     }
-    for (int k = k0; k < k1; k++) {
-        const MeshDev::BSide &S = M.bs[k];
-        if ((S.axis == 0 ? r.oy : r.ox) != S.c) continue;
-        const double u = S.axis == 0 ? r.ox : r.oy;
-        if (!(u > S.lo && u < S.hi)) return false;
-        int b = (int)((u - S.lo) * S.scale);
-        b = b < 0 ? 0 : (b >= S.nb ? S.nb - 1 : b);
-        int e = T.bbucket[S.boff + b];
-        double2 U = T.bu[S.off + e];
-        while (u >= U.y && e < S.cnt - 1) U = T.bu[S.off + (++e)];
-        if (!(U.x < u && u < U.y)) return false;  // on a vertex: general path
-        const double4 PQ = T.bpq[S.off + e];
-        const uint32_t word = (uint32_t)T.bword[S.off + e];
-        const double2 P = make_double2(PQ.x, PQ.y), Q = make_double2(PQ.z, PQ.w);
-        const double2 A = __ldg(M.cxy + word);  // apex corner j of T: cxy[3T + j], word = 3T + j
-        // _contains values in the reference's form: edge i -> (corner i+1, corner i+2)
-        const double ej = sa2(P, Q, r.ox, r.oy);
-        const double e1 = sa2(Q, A, r.ox, r.oy);
-        const double e2 = sa2(A, P, r.ox, r.oy);
-        if (!(ej >= -1e-15 && e1 > 1e-12 && e2 > 1e-12)) return false;
-        const double sa = side_of(r, P), sb = side_of(r, Q);
-        if (!(sb < 0.0 && 0.0 < sa)) return false;
+    ok = ok && k >= 0;
+    const MeshDev::BSide &S = M.bs[k < 0 ? 0 : k];
+    const double u = S.axis == 0 ? r.ox : r.oy;
+    ok = ok && u > S.lo && u < S.hi;
+    int b = (int)((u - S.lo) * S.scale);
+    b = b < 0 ? 0 : (b >= S.nb ? S.nb - 1 : b);
+    int e = T.bbucket[S.boff + b];
+    double2 U = T.bu[S.off + e];
+    while (ok && u >= U.y && e < S.cnt - 1) U = T.bu[S.off + (++e)];
+    ok = ok && U.x < u && u < U.y;  // strictly inside the edge (on a vertex: general path)
+    const double4 PQ = T.bpq[S.off + e];
+    const uint32_t word = (uint32_t)T.bword[S.off + e];
+    const double2 P = make_double2(PQ.x, PQ.y), Q = make_double2(PQ.z, PQ.w);
+    const double2 A = __ldg(M.cxy + word);  // apex corner j of T: cxy[3T + j], word = 3T + j
+    // _contains values in the reference's form: edge i -> (corner i+1, corner i+2)
+    const double ej = sa2(P, Q, r.ox, r.oy);
+    const double e1 = sa2(Q, A, r.ox, r.oy);
+    const double e2 = sa2(A, P, r.ox, r.oy);
+    const double sa = side_of(r, P), sb = side_of(r, Q);
+    ok = ok && ej >= -1e-15 && e1 > 1e-12 && e2 > 1e-12 && sb < 0.0 && 0.0 < sa;
+    if (ok) {
         s.w = word;
         s.sq = sa;  // side of corner (j+1)%3
         s.sp = sb;  // side of corner (j+2)%3
@@ -565,9 +567,8 @@ __device__ __forceinline__ bool boundary_start(const MeshDev &M, const BTab &T, 
         s.steps = 0;  // the first walk step enters (counts) T itself
         s.kr = (int)word;
         s.ch = 0;
-        return true;
     }
-    return false;
+    return ok;
 }
 
 // the walk words of triangle t's three edges: from the staged walk table when
@@ -589,7 +590,8 @@ __device__ __forceinline__ Init prologue_body(const MeshDev &M, const BTab &T, c
     const Ray r = GEN ? gen_ray(src.mode, src.box, src.key, src.first + (unsigned long long)i)
                       : load_ray(src.rays, i);
     o.ox = r.ox; o.oy = r.oy; o.dx = r.dx; o.dy = r.dy;
-    if (!src.start) {
+    // (generated interior rays never start on the box: skip the table)
+    if (!src.start && !(GEN && src.mode == MWT_RAYS_INTERIOR)) {
         WalkState bs;
         if (boundary_start(M, T, r, bs)) {
             o.start = bs.kr / 3;
