@@ -222,13 +222,10 @@ __device__ __forceinline__ Ray gen_ray(int mode, const Box &b, unsigned long lon
         // through the side facing -d in x with probability H|dx| / (H|dx| + W|dy|),
         // else through the side facing -d in y, uniformly along that side
         const double wx = H * fabs(r.dx), wy = W * fabs(r.dy);
-        if (u * (wx + wy) < wx) {
-            r.ox = r.dx > 0.0 ? b.x0 : b.x1;
-            r.oy = b.y0 + H * v;
-        } else {
-            r.oy = r.dy > 0.0 ? b.y0 : b.y1;
-            r.ox = b.x0 + W * v;
-        }
+        const bool xside = u * (wx + wy) < wx;  // (selects, not a divergent branch)
+        const double along = xside ? b.y0 + H * v : b.x0 + W * v;
+        r.ox = xside ? (r.dx > 0.0 ? b.x0 : b.x1) : along;
+        r.oy = xside ? along : (r.dy > 0.0 ? b.y0 : b.y1);
     }
     return r;
 }
