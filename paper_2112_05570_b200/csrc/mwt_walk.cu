@@ -661,6 +661,7 @@ __device__ __forceinline__ InitP prologue(long long i, const Launch *__restrict_
 struct HistSm {
     unsigned int bins[MWT_HIST_LEN];
     unsigned long long steps_sum;
+    unsigned long long warp_steps[32];  // per-warp partial step sums (owner-only updates)
 };
 
 __device__ __forceinline__ void hist_add_warp(HistSm *H, int seg, int steps, uint32_t st) {
@@ -674,7 +675,7 @@ __device__ __forceinline__ void hist_add_warp(HistSm *H, int seg, int steps, uin
     if (lane == leader) {
         if (hits) atomicAdd(H->bins + MWT_HIST_HIT, (unsigned)__popc(hits));
         if (m & ~hits) atomicAdd(H->bins + MWT_HIST_MISS, (unsigned)__popc(m & ~hits));
-        atomicAdd(&H->steps_sum, (unsigned long long)ssum);
+        H->warp_steps[threadIdx.x >> 5] += (unsigned long long)ssum;  // own slot: no atomic
     }
     while (any) {
         const int b = __ffs(any) - 1;
@@ -764,6 +765,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         for (int k = threadIdx.x; k < MWT_HIST_LEN; k += THREADS) H.bins[k] = 0u;
     if (threadIdx.x == 0) {
         H.steps_sum = 0ull;
+        for (int w = 0; w < 32; w++) H.warp_steps[w] = 0ull;
         s_next = (unsigned long long)cbeg;
     }
     __syncthreads();
@@ -889,8 +891,11 @@ __global__ void __launch_bounds__(THREADS, MINB)
         for (int k = threadIdx.x; k < MWT_HIST_LEN; k += THREADS)
             if (H.bins[k] && k != MWT_HIST_STEPS_SUM)
                 atomicAdd(reinterpret_cast<unsigned long long *>(hist + k), (unsigned long long)H.bins[k]);
-        if (threadIdx.x == 0 && H.steps_sum)
-            atomicAdd(reinterpret_cast<unsigned long long *>(hist + MWT_HIST_STEPS_SUM), H.steps_sum);
+        if (threadIdx.x == 0) {
+            unsigned long long t = H.steps_sum;
+            for (int w = 0; w < THREADS / 32; w++) t += H.warp_steps[w];
+            if (t) atomicAdd(reinterpret_cast<unsigned long long *>(hist + MWT_HIST_STEPS_SUM), t);
+        }
     }
 }
 
