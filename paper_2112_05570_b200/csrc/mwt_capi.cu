@@ -202,6 +202,7 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     m->dev.bo_bpq = (int32_t)bo_bpq;
     m->dev.bo_bword = (int32_t)bo_bword;
     m->dev.bo_bbucket = (int32_t)bo_bbucket;
+    m->dev.gseg_staged = (int64_t)bblob_bytes + 32LL * P.ns <= mwt::kSmemWalkMax;
     if (!P.crec.empty()) {
         m->dev.crec = reinterpret_cast<const uint2 *>(crec);
         m->dev.vxy = reinterpret_cast<const double2 *>(vxy);

@@ -136,6 +136,7 @@ struct MeshDev {
     const uint4 *bblob;
     int32_t bblob_bytes, bo_bpq, bo_bword, bo_bbucket;
     int32_t seg_staged;  // the segments (32 B each) also fit: staged after the blob
+    int32_t gseg_staged;  // without the walk table: the segments fit after the blob
 };
 
 struct BvhDev {

@@ -726,7 +726,7 @@ constexpr int kGrab = 128;  // rays a warp takes from its CTA's counter at a tim
 // SMEM: the compact walk table (mwt_internal.h) is staged into shared memory
 // once per CTA and the tight loop reads it there (one CTA of THREADS per SM);
 // otherwise the tight loop reads the 32-B step records from global memory.
-template <bool GEN, int MINB, int THREADS, bool SMEM>
+template <bool GEN, int MINB, int THREADS, bool SMEM, bool STAGE = SMEM>
 __global__ void __launch_bounds__(THREADS, MINB)
     k_trace(const __grid_constant__ MeshDev M, const __grid_constant__ Launch L, long long n,
             long long *hist, int refill_below) {
@@ -737,22 +737,27 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const double2 *svxy = reinterpret_cast<const double2 *>(dsm + (SMEM ? M.crec_bytes : 0));
     BTab btab{M.bu, M.bpq, M.bword, M.bbucket, nullptr, nullptr};
     const double4 *sseg = nullptr;
+    const int wbytes = SMEM ? M.smem_bytes : 0;  // the walk table, then the boundary blob, segments
     if (SMEM) {
-        const int n16 = M.smem_bytes >> 4, c16 = M.crec_bytes >> 4, b16 = M.bblob_bytes >> 4;
+        const int n16 = M.smem_bytes >> 4, c16 = M.crec_bytes >> 4;
         uint4 *d = reinterpret_cast<uint4 *>(dsm);
         const uint4 *a = reinterpret_cast<const uint4 *>(M.crec);
         const uint4 *b = reinterpret_cast<const uint4 *>(M.vxy);
         for (int k = threadIdx.x; k < n16; k += THREADS) d[k] = k < c16 ? __ldg(a + k) : __ldg(b + (k - c16));
-        for (int k = threadIdx.x; k < b16; k += THREADS) d[n16 + k] = __ldg(M.bblob + k);
-        const unsigned char *bb = dsm + M.smem_bytes;
+        btab.srec = srec;
+        btab.svxy = svxy;
+    }
+    if (STAGE) {
+        const int b16 = M.bblob_bytes >> 4;
+        uint4 *d = reinterpret_cast<uint4 *>(dsm + wbytes);
+        for (int k = threadIdx.x; k < b16; k += THREADS) d[k] = __ldg(M.bblob + k);
+        const unsigned char *bb = dsm + wbytes;
         btab.bu = reinterpret_cast<const double2 *>(bb);
         btab.bpq = reinterpret_cast<const double4 *>(bb + M.bo_bpq);
         btab.bword = reinterpret_cast<const int32_t *>(bb + M.bo_bword);
         btab.bbucket = reinterpret_cast<const int32_t *>(bb + M.bo_bbucket);
-        btab.srec = srec;
-        btab.svxy = svxy;
-        if (M.seg_staged) {
-            uint4 *ds = reinterpret_cast<uint4 *>(dsm + M.smem_bytes + M.bblob_bytes);
+        if (SMEM ? M.seg_staged : M.gseg_staged) {
+            uint4 *ds = reinterpret_cast<uint4 *>(dsm + wbytes + M.bblob_bytes);
             const uint4 *gs = reinterpret_cast<const uint4 *>(M.seg);
             for (int k = threadIdx.x; k < 2 * M.ns; k += THREADS) ds[k] = __ldg(gs + k);
             sseg = reinterpret_cast<const double4 *>(ds);
@@ -979,13 +984,14 @@ static int persistent_grid(K kernel, long long n, int threads = kThreads, int sm
 
 constexpr int kSmemThreads = 1024;  // one CTA per SM shares the staged table
 
-template <bool GEN, int MINB, int THREADS, bool SMEM>
+template <bool GEN, int MINB, int THREADS, bool SMEM, bool STAGE = SMEM>
 static bool launch_k_trace(const MeshDev &m, const Launch &L, long long n, long long *hist,
                            void *stream) {
-    auto kern = k_trace<GEN, MINB, THREADS, SMEM>;
-    const int dyn = SMEM ? m.smem_bytes + m.bblob_bytes + (m.seg_staged ? 32 * m.ns : 0) : 0;
-    if (SMEM) {
-        if (m.smem_bytes <= 0) return false;  // the walk table does not fit: variant 1
+    auto kern = k_trace<GEN, MINB, THREADS, SMEM, STAGE>;
+    const int dyn = SMEM ? m.smem_bytes + m.bblob_bytes + (m.seg_staged ? 32 * m.ns : 0)
+                  : STAGE ? m.bblob_bytes + (m.gseg_staged ? 32 * m.ns : 0) : 0;
+    if (SMEM && m.smem_bytes <= 0) return false;  // the walk table does not fit: variant 1
+    if (STAGE) {
         int dev = 0;
         cudaGetDevice(&dev);
         if (dev < 0 || dev >= 64) return false;
@@ -1012,6 +1018,8 @@ static void launch_k_trace_any(const MeshDev &m, const Launch &L, long long n, l
                               : launch_k_trace<GEN, 1, kSmemThreads, true>(m, L, n, hist, stream))
             return;
     }
+    // global walk records; boundary table (and segments when they fit) staged
+    if (g_min_blocks == 3 && launch_k_trace<GEN, 1, 768, false, true>(m, L, n, hist, stream)) return;
     if (g_min_blocks == 3)
         launch_k_trace<GEN, 3, kThreads, false>(m, L, n, hist, stream);
     else if (g_min_blocks == 2)
