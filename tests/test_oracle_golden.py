@@ -157,3 +157,29 @@ def test_structures_golden(cfg):
         assert np.array_equal(o["ropes"][ok], g[f"kd{tag}_ropes"][ok])
         assert np.array_equal(o["prims"][ok], g[f"kd{tag}_prims"][ok])
         assert np.array_equal((o["status"] & 1) == 1, ~ok)
+
+
+@pytest.mark.parametrize("box", [(0.0, 0.0, 1.0, 1.0), (0.0, 0.0, 1.0, 0.5)])
+def test_raygen_box_entry_is_a_uniform_line_field(box):
+    """BASELINE.json's ray recipe: isotropic lines with a uniform perpendicular
+    offset over the box's projected width, origin at the box entry point.
+    Within each direction bin, the offset n.o (n = (-dy, dx)) normalised to the
+    box's projection must be uniform, and every origin lies on the side that
+    faces -d."""
+    from scipy.stats import kstest
+    x0, y0, x1, y1 = box
+    r = rg.raygen(0, box, 11, 0, 400000)
+    ox, oy, dx, dy = r.T
+    on_side = ((ox == x0) & (dx > 0)) | ((ox == x1) & (dx < 0)) | ((oy == y0) & (dy > 0)) | \
+        ((oy == y1) & (dy < 0))
+    assert on_side.all()
+    ang = np.arctan2(dy, dx)
+    cx = np.array([x0, x1, x1, x0])
+    cy = np.array([y0, y0, y1, y1])
+    for lo in np.linspace(-np.pi, np.pi, 8, endpoint=False):
+        sel = (ang >= lo) & (ang < lo + np.pi / 4)
+        nx, ny = -dy[sel], dx[sel]
+        s = nx * ox[sel] + ny * oy[sel]
+        proj = nx[:, None] * cx[None, :] + ny[:, None] * cy[None, :]
+        a, b = proj.min(1), proj.max(1)
+        assert kstest((s - a) / (b - a), "uniform").pvalue > 1e-4, lo
