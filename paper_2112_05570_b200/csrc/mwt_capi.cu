@@ -59,7 +59,7 @@ T *carve(Arena &a, size_t count) {
 
 }  // namespace
 
-constexpr int kHostStreams = 4;
+constexpr int kHostStreams = 8;
 constexpr int64_t kHostChunk = 1 << 19;  // rays per pipelined chunk of mwt_trace_host
 
 struct mwt_mesh {
