@@ -2,13 +2,16 @@
 // for B200 (sm_100a).  Compiled with -fmad=false: every fp64 expression is
 // evaluated in the reference's operation order with no contraction.
 //
-// Execution model (K4): persistent warps.  Each warp owns a contiguous chunk
-// of ray indices; a lane whose ray has terminated goes idle, and once at most
-// `refill_below` lanes of the warp are still walking, all idle lanes fetch the
-// next rays of the chunk together (ballot + popc rank), generate / load them,
-// locate their start triangle and enter the walk.  Walk steps therefore run
-// with most lanes busy, and the expensive per-ray prologue (raygen + locate)
-// runs with many lanes at once.
+// Execution model (K4): one persistent CTA per SM (768 threads, 80
+// registers).  The CTA stages the mesh's compact walk table, the boundary-edge
+// table and the segments in shared memory when they fit, owns a contiguous
+// range of rays and hands them to its warps 128 at a time.  In a warp, a lane
+// whose ray has terminated goes idle; once at most `refill_below` lanes are
+// still walking, the finished lanes run the epilogue (hit test, outputs,
+// histogram) and the idle lanes the prologue of their next rays (raygen or
+// load, box-entry start or locate, first triangle) as one batch.  Between
+// batches the walking lanes run a predicated loop of one-candidate steps.
+// Everything is inlined: out-of-line calls spilled ~140 B per ray.
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
