@@ -726,6 +726,46 @@ constexpr int kGrab = 128;  // rays a warp takes from its CTA's counter at a tim
 // lanes are still walking, the lanes whose rays ended run the epilogue and
 // the idle lanes the prologue of the next rays, both as one batch.
 //
+// ---------------------------------------------------------------------------
+// Staging with the bulk-copy engine (cp.async.bulk, the 1-D TMA path): one
+// thread arms an mbarrier with the byte count and issues the copies; every
+// thread waits on the barrier's phase.  Sizes and addresses are multiples of 16.
+
+__device__ __forceinline__ unsigned smem_u32(const void *p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes,
+                                         unsigned long long *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        :: "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+
+// stage n pieces (dst, src, bytes) into shared memory; call from all threads
+__device__ __forceinline__ void bulk_stage(unsigned long long *bar, int n, void *const *dst,
+                                           const void *const *src, const unsigned *bytes) {
+    if (threadIdx.x == 0) {
+        unsigned total = 0;
+        for (int k = 0; k < n; k++) total += bytes[k];
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(bar)) : "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                     :: "r"(smem_u32(bar)), "r"(total) : "memory");
+        for (int k = 0; k < n; k++)
+            for (unsigned off = 0; off < bytes[k]; off += 65536u) {
+                const unsigned b = bytes[k] - off < 65536u ? bytes[k] - off : 65536u;
+                bulk_g2s(static_cast<char *>(dst[k]) + off, static_cast<const char *>(src[k]) + off, b,
+                         bar);
+            }
+    }
+    __syncthreads();  // the barrier is initialised
+    asm volatile(
+        "{\n.reg .pred p;\nLAB_WAIT%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+        "@!p bra LAB_WAIT%=;\n}\n" :: "r"(smem_u32(bar)) : "memory");
+}
+
 // SMEM: the compact walk table (mwt_internal.h) is staged into shared memory
 // once per CTA and the tight loop reads it there (one CTA of THREADS per SM);
 // otherwise the tight loop reads the 32-B step records from global memory.
@@ -741,30 +781,33 @@ __global__ void __launch_bounds__(THREADS, MINB)
     BTab btab{M.bu, M.bpq, M.bword, M.bbucket, nullptr, nullptr};
     const double4 *sseg = nullptr;
     const int wbytes = SMEM ? M.smem_bytes : 0;  // the walk table, then the boundary blob, segments
-    if (SMEM) {
-        const int n16 = M.smem_bytes >> 4, c16 = M.crec_bytes >> 4;
-        uint4 *d = reinterpret_cast<uint4 *>(dsm);
-        const uint4 *a = reinterpret_cast<const uint4 *>(M.crec);
-        const uint4 *b = reinterpret_cast<const uint4 *>(M.vxy);
-        for (int k = threadIdx.x; k < n16; k += THREADS) d[k] = k < c16 ? __ldg(a + k) : __ldg(b + (k - c16));
-        btab.srec = srec;
-        btab.svxy = svxy;
-    }
-    if (STAGE) {
-        const int b16 = M.bblob_bytes >> 4;
-        uint4 *d = reinterpret_cast<uint4 *>(dsm + wbytes);
-        for (int k = threadIdx.x; k < b16; k += THREADS) d[k] = __ldg(M.bblob + k);
-        const unsigned char *bb = dsm + wbytes;
-        btab.bu = reinterpret_cast<const double2 *>(bb);
-        btab.bpq = reinterpret_cast<const double4 *>(bb + M.bo_bpq);
-        btab.bword = reinterpret_cast<const int32_t *>(bb + M.bo_bword);
-        btab.bbucket = reinterpret_cast<const int32_t *>(bb + M.bo_bbucket);
-        if (SMEM ? M.seg_staged : M.gseg_staged) {
-            uint4 *ds = reinterpret_cast<uint4 *>(dsm + wbytes + M.bblob_bytes);
-            const uint4 *gs = reinterpret_cast<const uint4 *>(M.seg);
-            for (int k = threadIdx.x; k < 2 * M.ns; k += THREADS) ds[k] = __ldg(gs + k);
-            sseg = reinterpret_cast<const double4 *>(ds);
+    if (SMEM || STAGE) {
+        __shared__ __align__(8) unsigned long long stage_bar;
+        void *dst[4];
+        const void *src[4];
+        unsigned bytes[4];
+        int np = 0;
+        if (SMEM) {
+            dst[np] = dsm; src[np] = M.crec; bytes[np++] = (unsigned)M.crec_bytes;
+            dst[np] = dsm + M.crec_bytes; src[np] = M.vxy;
+            bytes[np++] = (unsigned)(M.smem_bytes - M.crec_bytes);
+            btab.srec = srec;
+            btab.svxy = svxy;
         }
+        if (STAGE) {
+            const unsigned char *bb = dsm + wbytes;
+            dst[np] = dsm + wbytes; src[np] = M.bblob; bytes[np++] = (unsigned)M.bblob_bytes;
+            btab.bu = reinterpret_cast<const double2 *>(bb);
+            btab.bpq = reinterpret_cast<const double4 *>(bb + M.bo_bpq);
+            btab.bword = reinterpret_cast<const int32_t *>(bb + M.bo_bword);
+            btab.bbucket = reinterpret_cast<const int32_t *>(bb + M.bo_bbucket);
+            if (SMEM ? M.seg_staged : M.gseg_staged) {
+                dst[np] = dsm + wbytes + M.bblob_bytes; src[np] = M.seg;
+                bytes[np++] = 32u * (unsigned)M.ns;
+                sseg = reinterpret_cast<const double4 *>(dsm + wbytes + M.bblob_bytes);
+            }
+        }
+        bulk_stage(&stage_bar, np, dst, src, bytes);
     }
     const long long per = (n + gridDim.x - 1) / gridDim.x;
     const long long cbeg = (long long)blockIdx.x * per;
