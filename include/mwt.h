@@ -89,7 +89,7 @@ const char *mwt_last_error(void);
 int mwt_device_count(int *count);
 /* Tuning knobs of the persistent walk kernel (process-wide; -1 = keep).
  * Lanes whose rays ended refill in one batch once at most `refill_below`
- * (default 4) lanes of the warp still walk.  `variant` 2 (default) stages the
+ * (default 6) lanes of the warp still walk.  `variant` 2 (default) stages the
  * mesh's compact walk table in shared memory (1024-thread CTAs, one per SM)
  * when it fits, else runs variant 1: walk records read from global memory,
  * 256-thread CTAs, `min_blocks_per_sm` in {2,3,4} selecting the register

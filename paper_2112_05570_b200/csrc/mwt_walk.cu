@@ -995,7 +995,7 @@ __global__ void __launch_bounds__(kThreads) k_histogram(const int32_t *seg, cons
 
 #define MWT_LAUNCH_RET return (int)cudaGetLastError()
 
-static int g_refill_below = 4;  // tuned on B200 (tools/tune.py): refill late, walk long
+static int g_refill_below = 6;  // tuned on B200 (tools/breakdown.py): refill when <= 6 lanes still walk
 static int g_min_blocks = 3;    // 3: 80 registers (variant 1: 3 CTAs x 256; variant 2: 768-thread CTA); 4: 64
 static int g_variant = 2;       // 2: shared-memory staged walk when the compact table fits, else 1
 

@@ -118,7 +118,7 @@ def test_tuning_knobs_do_not_change_results(cfg, refill, minb, variant):
     try:
         got = m.trace(rays)
     finally:
-        _lib.lib.mwt_set_tuning(4, 3, 2)  # the defaults
+        _lib.lib.mwt_set_tuning(6, 3, 2)  # the defaults
     for k in ("start", "seg", "steps"):
         assert np.array_equal(got[k], ref[k])
 
