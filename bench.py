@@ -4,7 +4,8 @@ Workload (BASELINE.json configs[1], Lines-1024): per GPU and step, 2^24
 isotropic box-entry rays plus 2^22 'recursive' rays with interior origins,
 each generated on device (K2), located (K3), walked through the annealed MWT
 (K4) with per-ray results written to HBM and step/hit histograms accumulated
-(K7); for N > 1 the histograms are summed with one NCCL all-reduce.  Rays are
+(K7); the two parts run on two streams (one part's tail overlaps the other's
+start); for N > 1 the histograms are summed with one NCCL all-reduce.  Rays are
 sharded by global index (rank r traces indices [r*n, (r+1)*n)), so per-GPU
 work is fixed: weak scaling.  The L2 is flushed (256 MiB write) before every
 timed step, outside the timed region.
@@ -235,14 +236,32 @@ def main():
 
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in parts]
 
+    # the parts run on their own streams, so one part's tail overlaps the next
+    # part's start (each kernel keeps one CTA per SM)
+    pstreams = [stream] + [torch.cuda.Stream(device=dev) for _ in parts[1:]]
+    pptrs = [sptr] + [_stream(ps) for ps in pstreams[1:]]
+    zero_done = torch.cuda.Event()
+
+    def launch_on(k, mode, n, h):
+        o = outs[mode]
+        _lib.check(_lib.lib.mwt_trace_generated_dev(
+            mesh.handle, mode, P(boxarr), SEED, rank * n, n,
+            P(o["seg"]), P(o["t"]), P(o["steps"]), P(h), pptrs[k]), "trace_generated")
+
     def step(timed_kernels=None):
         hist.zero_()
+        zero_done.record(stream)
         for k, (mode, n) in enumerate(parts):
+            ps = pstreams[k]
+            if k:
+                ps.wait_event(zero_done)
             if timed_kernels is not None:
-                ev[k][0].record(stream)
-            launch(mode, n, hist)
+                ev[k][0].record(ps)
+            launch_on(k, mode, n, hist)
             if timed_kernels is not None:
-                ev[k][1].record(stream)
+                ev[k][1].record(ps)
+        for ps in pstreams[1:]:
+            stream.wait_stream(ps)
         if world > 1:
             dist.all_reduce(hist)
 
