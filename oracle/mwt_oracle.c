@@ -13,7 +13,8 @@
  *   geometry.py:56-59   Segment.param_of
  *   accel.py:64-98      SceneIndex / canonical
  *   accel.py:101-132    brute_force_closest
- *   accel.py:138-213    traverse_triangulation
+ *   accel.py:138-213    traverse_triangulation (orc_trace_ex also returns the
+ *                       final triangle: the loop variable `cur` when it returns)
  *   accel.py:219-353    _contains, _resolve_tie, locate_brute_force, TriLocator
  *   trimesh.py:386-436  Triangulation.locate (anchor seeds)
  *   accel.py:460-518    _ray_box, bvh_intersect

@@ -16,6 +16,7 @@
 #include <math_constants.h>
 
 #include <cstdint>
+#include <mutex>
 
 #include "mwt_device.cuh"
 
@@ -999,9 +1000,14 @@ static int g_refill_below = 6;  // tuned on B200 (tools/breakdown.py): refill wh
 static int g_min_blocks = 3;    // 3: 80 registers (variant 1: 3 CTAs x 256; variant 2: 768-thread CTA); 4: 64
 static int g_variant = 2;       // 2: shared-memory staged walk when the compact table fits, else 1
 
+// the launch-configuration caches below are process-wide: calls from several
+// host threads (one per device or stream) serialise on this lock
+static std::mutex g_cfg_mu;
+
 template <typename K>
 static int persistent_grid(K kernel, long long n, int threads = kThreads, int smem = 0) {
     // one resident wave: SMs x resident CTAs (cached per kernel, device, smem size)
+    std::lock_guard<std::mutex> lk(g_cfg_mu);
     static const void *keys[64];
     static int devs[64], smems[64], waves[64], nkeys = 0;
     int dev = 0;
@@ -1042,6 +1048,7 @@ static bool launch_k_trace(const MeshDev &m, const Launch &L, long long n, long 
         cudaGetDevice(&dev);
         if (dev < 0 || dev >= 64) return false;
         static int attr_set[64] = {};  // per instantiation and device: enabled dynamic size
+        std::lock_guard<std::mutex> lk(g_cfg_mu);
         if (attr_set[dev] < dyn) {
             if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) !=
                 cudaSuccess) {
