@@ -527,6 +527,7 @@ struct BTab {  // the boundary-edge table arrays (global or a shared-memory copy
     const double2 *bu;
     const double4 *bpq;
     const int32_t *bword, *bbucket;
+    const MeshDev::BSide *bs;  // the side descriptors (shared-memory copy: lanes index freely)
     const uint2 *srec;  // the staged walk table (corners for locate), or NULL
     const double2 *svxy;
 };
@@ -544,7 +545,7 @@ __device__ __forceinline__ bool boundary_start(const MeshDev &M, const BTab &T, 
             if ((M.bs[kk].axis == 0 ? r.oy : r.ox) == M.bs[kk].c) k = kk;
     }
     ok = ok && k >= 0;
-    const MeshDev::BSide &S = M.bs[k < 0 ? 0 : k];
+    const MeshDev::BSide &S = T.bs[k < 0 ? 0 : k];
     const double u = S.axis == 0 ? r.ox : r.oy;
     ok = ok && u > S.lo && u < S.hi;
     int b = (int)((u - S.lo) * S.scale);
@@ -779,7 +780,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
     extern __shared__ __align__(16) unsigned char dsm[];
     const uint2 *srec = reinterpret_cast<const uint2 *>(dsm);
     const double2 *svxy = reinterpret_cast<const double2 *>(dsm + (SMEM ? M.crec_bytes : 0));
-    BTab btab{M.bu, M.bpq, M.bword, M.bbucket, nullptr, nullptr};
+    __shared__ MeshDev::BSide sbs[4];
+    if (threadIdx.x < 4) sbs[threadIdx.x] = M.bs[threadIdx.x];
+    BTab btab{M.bu, M.bpq, M.bword, M.bbucket, sbs, nullptr, nullptr};
     const double4 *sseg = nullptr;
     const int wbytes = SMEM ? M.smem_bytes : 0;  // the walk table, then the boundary blob, segments
     if (SMEM || STAGE) {
