@@ -301,13 +301,15 @@ int pack_mesh(const double *vx, const double *vy, int32_t nv, const int32_t *tv,
     for (int k = 0; k < nv; k++)
         if (!(std::fabs(vx[k]) <= 4.0 && std::fabs(vy[k]) <= 4.0)) P.flood_filter = 0;
     // seed grid: the reference's TriLocator uses max(2, int(sqrt(T/2))) cells
-    // per side (accel.py:265-266); the device uses a 12x finer grid (~72 cells
-    // per triangle, 1.2 MB for Lines-1024, L2-resident) so the seed cell's
-    // triangle usually contains the origin (measured: 3x finer than 4x took 6%
-    // off the interior-ray launch).  Any containing triangle seeds the same
-    // lowest-id flood (accel.py:226-238).
+    // per side (accel.py:265-266); the device uses a 24x finer grid (~290 cells
+    // per triangle; Lines-1024: 1080^2 cells, 4.7 MB, L2-resident) so the seed
+    // cell's triangle almost always contains the origin (measured on the
+    // interior-ray launch: 4x -> 12x -6%, 12x -> 24x -3%), capped at 2^23
+    // cells.  Any containing triangle seeds the same lowest-id flood
+    // (accel.py:226-238).
     int ntc = nt > 4 ? nt : 4;
-    int res = 12 * (int)std::sqrt(ntc / 2.0);
+    int res = 24 * (int)std::sqrt(ntc / 2.0);
+    if ((long long)res * res > (1LL << 23)) res = 2896;  // floor(sqrt(2^23))
     if (res < 2) res = 2;
     P.res = res;
     P.anchor.assign((size_t)res * res, 0);
