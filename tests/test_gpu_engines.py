@@ -159,6 +159,13 @@ def test_edge_cases():
     assert np.array_equal(got["status"].view(np.uint32) & mask, ref["status"] & mask)
     hit = ok & (ref["seg"] >= 0)
     assert np.array_equal(got["t"][hit], ref["t"][hit])
+    # non-finite rays and origins far outside the mesh: terminate, no hang
+    odd = np.array([[np.nan, 0.5, 1.0, 0.0], [0.5, 0.5, np.nan, 1.0], [np.inf, 0.5, -1.0, 0.0],
+                    [0.5, 0.5, np.inf, 0.0], [1e6, -1e6, 0.6, 0.8], [-3.0, 0.5, 1.0, 0.0],
+                    [0.5, 0.5, 0.0, 0.0]], np.float64)
+    o2 = m.trace(odd)
+    assert len(o2["seg"]) == len(odd)
+    assert (o2["steps"] >= 0).all() and (o2["steps"] <= 4 * tri.v.shape[0] + 16).all()
 
 
 def test_full_size_floorplan_properties():
