@@ -440,7 +440,9 @@ int mwt_bvh_create(const mwt_mesh *mesh, int32_t nnodes, const double *box, cons
         delete b;
         return cuda_fail(e, "bvh_create: upload");
     }
-    b->dev = mwt::BvhDev{nnodes, dbox, dch, dpr, dpm};
+    b->dev = mwt::BvhDev{nnodes, dbox, dch, dpr, dpm, a.base, (int32_t)bytes,
+                         (int32_t)((char *)dch - (char *)a.base), (int32_t)((char *)dpr - (char *)a.base),
+                         (int32_t)((char *)dpm - (char *)a.base)};
     *out = b;
     return MWT_OK;
 }

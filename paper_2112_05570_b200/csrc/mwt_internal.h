@@ -145,6 +145,9 @@ struct BvhDev {
     const int2 *child;     // (left, right), left < 0 => leaf
     const int2 *prange;    // (prim_off, prim_cnt)
     const int32_t *prims;
+    // the four arrays as one blob (box at 0), for staging in shared memory
+    const void *blob;
+    int32_t blob_bytes, o_child, o_prange, o_prims;
 };
 
 struct KdDev {

@@ -37,10 +37,32 @@ __device__ __forceinline__ bool ray_box(const Ray &r, double4 b, double &tn) {
     return true;
 }
 
+// STAGE: the tree (one blob) and the segments are copied into shared memory
+// once per CTA (persistent grid-stride CTAs), as the walk kernel stages its
+// tables -- the like-for-like comparison reads its structure on chip too.
+template <bool STAGE>
 __global__ void __launch_bounds__(kThreads) k_bvh(MeshDev M, BvhDev B, const double *rays,
                                                   long long n, int32_t *o_seg, double *o_t,
                                                   double *o_u, int32_t *o_nodes, int32_t *o_prims,
                                                   uint32_t *o_st) {
+    if (STAGE) {
+        extern __shared__ __align__(16) unsigned char bsm[];
+        const int nb = B.blob_bytes >> 4, ns2 = 2 * M.ns;
+        uint4 *d = reinterpret_cast<uint4 *>(bsm);
+        const uint4 *a = reinterpret_cast<const uint4 *>(B.blob);
+        const uint4 *sg = reinterpret_cast<const uint4 *>(M.seg);
+        for (int k = threadIdx.x; k < nb + ns2; k += blockDim.x)
+            d[k] = k < nb ? __ldg(a + k) : __ldg(sg + (k - nb));
+        __syncthreads();
+        B.box = reinterpret_cast<const double4 *>(bsm);
+        B.child = reinterpret_cast<const int2 *>(bsm + B.o_child);
+        B.prange = reinterpret_cast<const int2 *>(bsm + B.o_prange);
+        B.prims = reinterpret_cast<const int32_t *>(bsm + B.o_prims);
+    }
+    // the segments the leaf tests read (canonical keeps the global copy: the
+    // segment table itself, rarely read)
+    extern __shared__ __align__(16) unsigned char bsm2[];
+    const double4 *segs = STAGE ? reinterpret_cast<const double4 *>(bsm2 + B.blob_bytes) : M.seg;
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         Ray r = load_ray(rays, i);
@@ -50,7 +72,7 @@ __global__ void __launch_bounds__(kThreads) k_bvh(MeshDev M, BvhDev B, const dou
         double bt = 0.0, bu = 0.0, tn;
         int seg = -1;
         double ot = CUDART_NAN, ou = CUDART_NAN;
-        if (ray_box(r, ldg4d(B.box), tn)) {
+        if (ray_box(r, B.box[0], tn)) {
             double st_t[kBvhStack];
             int st_n[kBvhStack];
             int top = 0;
@@ -62,23 +84,23 @@ __global__ void __launch_bounds__(kThreads) k_bvh(MeshDev M, BvhDev B, const dou
                 double tnear = st_t[top];
                 int node = st_n[top];
                 if (have && tnear > bt + 1e-12) continue;
-                int2 ch = __ldg(B.child + node);
+                int2 ch = B.child[node];
                 if (ch.x < 0) {
-                    int2 pr = __ldg(B.prange + node);
+                    int2 pr = B.prange[node];
                     for (int k = 0; k < pr.y; k++) {
-                        int sid = __ldg(B.prims + pr.x + k);
+                        int sid = B.prims[pr.x + k];
                         prims++;
                         double t, u;
                         bool par = false;
-                        if (!rsi(r, ldg4d(M.seg + sid), t, u, par)) continue;
+                        if (!rsi(r, segs[sid], t, u, par)) continue;
                         if (!have || t < bt) { have = true; bt = t; bsid = sid; bu = u; }
                     }
                     continue;
                 }
                 double tl = 0.0, tr = 0.0;
                 nodes += 2;
-                bool hl = ray_box(r, ldg4d(B.box + ch.x), tl) && (!have || tl <= bt + 1e-12);
-                bool hr = ray_box(r, ldg4d(B.box + ch.y), tr) && (!have || tr <= bt + 1e-12);
+                bool hl = ray_box(r, B.box[ch.x], tl) && (!have || tl <= bt + 1e-12);
+                bool hr = ray_box(r, B.box[ch.y], tr) && (!have || tr <= bt + 1e-12);
                 if (top + 2 > kBvhStack) { st |= ST_OVERFLOW; break; }
                 // children sorted by tnear descending (stable) then pushed: the
                 // nearer pops first; on equal tnear the right child pops first
@@ -273,8 +295,26 @@ int launch_bvh(const MeshDev &m, const BvhDev &b, const double *rays, int64_t n,
                double *o_t, double *o_u, int32_t *o_nodes, int32_t *o_prims, uint32_t *o_st,
                void *stream) {
     if (n <= 0) return 0;
-    k_bvh<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(m, b, rays, n, o_seg, o_t, o_u,
-                                                              o_nodes, o_prims, o_st);
+    const int dyn = b.blob_bytes + 32 * m.ns;
+    if (dyn <= 200 * 1024) {
+        int dev = 0, sms = 0, per = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaFuncSetAttribute(k_bvh<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn) ==
+                cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_bvh<true>, kThreads, dyn) ==
+                cudaSuccess &&
+            per > 0) {
+            long long want = (n + kThreads - 1) / kThreads, wave = (long long)(sms > 0 ? sms : 148) * per;
+            const int grid = (int)(want < wave ? (want < 1 ? 1 : want) : wave);
+            k_bvh<true><<<grid, kThreads, dyn, (cudaStream_t)stream>>>(m, b, rays, n, o_seg, o_t, o_u,
+                                                                      o_nodes, o_prims, o_st);
+            MWT_LAUNCH_RET;
+        }
+        (void)cudaGetLastError();
+    }
+    k_bvh<false><<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(m, b, rays, n, o_seg, o_t, o_u,
+                                                                     o_nodes, o_prims, o_st);
     MWT_LAUNCH_RET;
 }
 
