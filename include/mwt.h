@@ -90,10 +90,11 @@ int mwt_device_count(int *count);
 /* Tuning knobs of the persistent walk kernel (process-wide; -1 = keep).
  * Lanes whose rays ended refill in one batch once at most `refill_below`
  * (default 6) lanes of the warp still walk.  `variant` 2 (default) stages the
- * mesh's compact walk table in shared memory (1024-thread CTAs, one per SM)
- * when it fits, else runs variant 1: walk records read from global memory,
- * 256-thread CTAs, `min_blocks_per_sm` in {2,3,4} selecting the register
- * budget (default 4 = 64 registers). */
+ * mesh's compact walk table in shared memory when it fits, one CTA per SM
+ * whose size `min_blocks_per_sm` picks (3: 768 threads / 80 registers,
+ * 4: 896 / 72 (default), 2: 1024 / 64), else walks the 32-B records from
+ * global memory with the boundary table staged (768 threads); variant 1 always
+ * walks from global memory with 256-thread CTAs, `min_blocks_per_sm` CTAs per SM. */
 int mwt_set_tuning(int refill_below, int min_blocks_per_sm, int variant);
 
 /* K1 -- mesh packer.

@@ -2,7 +2,7 @@
 // for B200 (sm_100a).  Compiled with -fmad=false: every fp64 expression is
 // evaluated in the reference's operation order with no contraction.
 //
-// Execution model (K4): one persistent CTA per SM (768 threads, 80
+// Execution model (K4): one persistent CTA per SM (896 threads, 72
 // registers).  The CTA stages the mesh's compact walk table, the boundary-edge
 // table and the segments in shared memory when they fit, owns a contiguous
 // range of rays and hands them to its warps 128 at a time.  In a warp, a lane
@@ -1000,7 +1000,7 @@ __global__ void __launch_bounds__(kThreads) k_histogram(const int32_t *seg, cons
 #define MWT_LAUNCH_RET return (int)cudaGetLastError()
 
 static int g_refill_below = 6;  // tuned on B200 (tools/breakdown.py): refill when <= 6 lanes still walk
-static int g_min_blocks = 3;    // 3: 80 registers (variant 1: 3 CTAs x 256; variant 2: 768-thread CTA); 4: 64
+static int g_min_blocks = 4;    // register budget; see launch_k_trace_any
 static int g_variant = 2;       // 2: shared-memory staged walk when the compact table fits, else 1
 
 // the launch-configuration caches below are process-wide: calls from several
@@ -1037,7 +1037,6 @@ static int persistent_grid(K kernel, long long n, int threads = kThreads, int sm
     return (int)(want < wave ? (want < 1 ? 1 : want) : wave);
 }
 
-constexpr int kSmemThreads = 1024;  // one CTA per SM shares the staged table
 
 template <bool GEN, int MINB, int THREADS, bool SMEM, bool STAGE = SMEM>
 static bool launch_k_trace(const MeshDev &m, const Launch &L, long long n, long long *hist,
@@ -1069,13 +1068,17 @@ static bool launch_k_trace(const MeshDev &m, const Launch &L, long long n, long 
 template <bool GEN>
 static void launch_k_trace_any(const MeshDev &m, const Launch &L, long long n, long long *hist,
                                void *stream) {
+    // shared-memory walk table: one CTA per SM; min_blocks picks its size
+    // (3: 768 threads / 80 registers, 4: 896 / 72 (default, measured best),
+    // 2: 1024 / 64)
     if (g_variant == 2) {
-        if (g_min_blocks == 3 ? launch_k_trace<GEN, 1, 768, true>(m, L, n, hist, stream)
-                              : launch_k_trace<GEN, 1, kSmemThreads, true>(m, L, n, hist, stream))
-            return;
+        const bool ok = g_min_blocks == 3   ? launch_k_trace<GEN, 1, 768, true>(m, L, n, hist, stream)
+                        : g_min_blocks == 2 ? launch_k_trace<GEN, 1, 1024, true>(m, L, n, hist, stream)
+                                            : launch_k_trace<GEN, 1, 896, true>(m, L, n, hist, stream);
+        if (ok) return;
     }
     // global walk records; boundary table (and segments when they fit) staged
-    if (g_min_blocks == 3 && launch_k_trace<GEN, 1, 768, false, true>(m, L, n, hist, stream)) return;
+    if (g_variant == 2 && launch_k_trace<GEN, 1, 768, false, true>(m, L, n, hist, stream)) return;
     if (g_min_blocks == 3)
         launch_k_trace<GEN, 3, kThreads, false>(m, L, n, hist, stream);
     else if (g_min_blocks == 2)

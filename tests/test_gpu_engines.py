@@ -105,7 +105,8 @@ def test_generated_kernel_equals_explicit_rays_and_histogram():
 @pytest.mark.parametrize("cfg,refill,minb,variant", [
     ("hair512", 0, 4, 1), ("hair512", 4, 3, 1), ("hair512", 16, 2, 1), ("hair512", 31, 4, 1),
     ("hair512", 4, 4, 2),  # table too large for shared memory: falls back to variant 1
-    ("lines1024", 0, 4, 2), ("lines1024", 4, 4, 2), ("lines1024", 31, 4, 2), ("lines1024", 4, 4, 1)])
+    ("lines1024", 0, 4, 2), ("lines1024", 4, 4, 2), ("lines1024", 31, 4, 2), ("lines1024", 4, 4, 1),
+    ("lines1024", 6, 3, 2), ("lines1024", 6, 2, 2), ("floorplan64", 6, 4, 2)])
 def test_tuning_knobs_do_not_change_results(cfg, refill, minb, variant):
     from oracle import oracle as orc
     from paper_2112_05570_b200 import _lib
@@ -118,7 +119,7 @@ def test_tuning_knobs_do_not_change_results(cfg, refill, minb, variant):
     try:
         got = m.trace(rays)
     finally:
-        _lib.lib.mwt_set_tuning(6, 3, 2)  # the defaults
+        _lib.lib.mwt_set_tuning(6, 4, 2)  # the defaults
     for k in ("start", "seg", "steps"):
         assert np.array_equal(got[k], ref[k])
 
