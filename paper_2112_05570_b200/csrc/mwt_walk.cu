@@ -638,29 +638,6 @@ __device__ __forceinline__ Init prologue_body(const MeshDev &M, const BTab &T, c
     return o;
 }
 
-// Runs in refill batches, many lanes at once.  Returns the state packed:
-// flags = phase | fast << 2 | ch << 3 | steps << 4 (steps is 0 or 1 here).
-// (Inlined: an out-of-line call saves and restores the caller's live
-// registers through local memory, ~140 B of L2 write traffic per ray.)
-struct InitP {
-    double ox, oy, dx, dy, sp, sq;
-    uint32_t w, st;
-    int kr;
-    uint32_t flags;
-};
-
-template <bool GEN>
-__device__ __forceinline__ InitP prologue(long long i, const Launch *__restrict__ L,
-                                       const MeshDev *__restrict__ Mg, const BTab &T) {
-    const Init in = prologue_body<GEN>(*Mg, T, L->src, i);
-    if (L->out.start) L->out.start[i] = in.start;
-    InitP o;
-    o.ox = in.ox; o.oy = in.oy; o.dx = in.dx; o.dy = in.dy; o.sp = in.sp; o.sq = in.sq;
-    o.w = in.w; o.st = in.st; o.kr = in.cur;
-    o.flags = (uint32_t)in.phase | (in.fast ? 4u : 0u) | ((uint32_t)in.ei << 3) | ((uint32_t)in.steps << 4);
-    return o;
-}
-
 // Block-private histogram: a shared atomic per lane for its step bin,
 // warp-aggregated updates for hit / miss / the step sum / each status bit present.
 struct HistSm {
@@ -867,14 +844,15 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     const long long i = rank < rem ? next + rank : nb + (rank - rem);
                     if (rank < rem || i < ne) {
                         idx = i;
-                        const InitP in = prologue<GEN>(i, &L, &M, btab);
+                        const Init in = prologue_body<GEN>(M, btab, L.src, i);
+                        if (!GEN && L.out.start) L.out.start[i] = in.start;
                         r.ox = in.ox; r.oy = in.oy; r.dx = in.dx; r.dy = in.dy;
-                        s.sp = in.sp; s.sq = in.sq; s.w = in.w; s.kr = in.kr;
+                        s.sp = in.sp; s.sq = in.sq; s.w = in.w; s.kr = in.cur;
                         st = in.st;
-                        phase = (int)(in.flags & 3u);
-                        s.fast = (in.flags & 4u) != 0;
-                        s.ch = (int)((in.flags >> 3) & 1u);
-                        s.steps = (int)(in.flags >> 4);
+                        phase = in.phase;
+                        s.fast = in.fast;
+                        s.ch = in.ei;
+                        s.steps = in.steps;
                     }
                 }
                 if (rem >= nidle) {
