@@ -1056,7 +1056,7 @@ static void launch_k_trace_any(const MeshDev &m, const Launch &L, long long n, l
         if (ok) return;
     }
     // global walk records; boundary table (and segments when they fit) staged
-    if (g_variant == 2 && launch_k_trace<GEN, 1, 768, false, true>(m, L, n, hist, stream)) return;
+    if (g_variant == 2 && launch_k_trace<GEN, 1, 896, false, true>(m, L, n, hist, stream)) return;
     if (g_min_blocks == 3)
         launch_k_trace<GEN, 3, kThreads, false>(m, L, n, hist, stream);
     else if (g_min_blocks == 2)
