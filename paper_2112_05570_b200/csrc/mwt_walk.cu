@@ -874,9 +874,9 @@ __global__ void __launch_bounds__(THREADS, MINB)
         // once the range is exhausted, until none remains.  A lane leaves on a
         // zero apex side (the general rule decides that step), at its stop
         // edge, or at the step guard (walk_step below flags the error).
+        bool fl = phase == 1 && s.fast && s.steps < lim;
         {
             const int thr = more ? refill_below : 0;
-            bool fl = phase == 1 && s.fast && s.steps < lim;
             while (__popc(__ballot_sync(FULL, fl)) > thr) {
 #pragma unroll
                 for (int u2 = 0; u2 < 4; u2++) {
@@ -912,9 +912,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
             }
         }
         if (SMEM && (s.w & (kStopBit | kCStop)) == kCStop) s.w = expand_cword(s.w);
-        // one full-rule step for every lane still walking (zero sides, the
-        // general state, the guard, and the lanes the tight loop left behind)
-        if (phase == 1) {
+        // one full-rule step for every lane that left the tight loop still
+        // walking (zero side, the general state, the guard); lanes it merely
+        // left behind (still in the fast state) continue after the refill
+        if (phase == 1 && !fl) {
             if (!walk_step(M, r, s, st)) phase = 3;
             else if (s.w & kStopBit) phase = 2;
         }
