@@ -879,7 +879,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             const int thr = more ? refill_below : 0;
             while (__popc(__ballot_sync(FULL, fl)) > thr) {
 #pragma unroll
-                for (int u2 = 0; u2 < 4; u2++) {
+                for (int u2 = 0; u2 < 5; u2++) {
                     // predicated, not branched: lanes that left compute on record 0
                     // and commit nothing
                     const uint32_t k = fl ? s.w : 0u;
