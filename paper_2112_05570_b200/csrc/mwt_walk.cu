@@ -69,14 +69,6 @@ __device__ __forceinline__ bool inside(double e0, double e1, double e2) {
     return e0 >= -1e-15 && e1 >= -1e-15 && e2 >= -1e-15;
 }
 
-__device__ __forceinline__ bool contains_t(const MeshDev &M, int t, double px, double py) {
-    double2 P0, P1, P2;
-    corners(M, t, P0, P1, P2);
-    double e0, e1, e2;
-    edge_areas(P0, P1, P2, px, py, e0, e1, e2);
-    return inside(e0, e1, e2);
-}
-
 // locate_brute_force, accel.py:241-253.  Cold path: arguments by value so no
 // caller state becomes address-taken.
 struct LocRes {
@@ -420,36 +412,6 @@ __device__ __forceinline__ int walk_terminal(const MeshDev &M, const Ray &r, con
     const int s2 = canonical(M, r, sid, t, u, ot, ou);
     if (s2 != sid) st |= ST_CANON;
     return s2;
-}
-
-struct Term {
-    int seg;
-    uint32_t st;
-    double t, u;
-};
-
-// out-of-line epilogue: runs in batches at refill time
-// (everything by value: a reference to kernel-scope state would force that
-// state into local memory for the whole loop)
-__device__ __noinline__ Term terminal(const double4 *seg, const int2 *ep_range, const int32_t *ep_ids,
-                                      const double2 *cxy, double ox, double oy, double dx, double dy,
-                                      int kr, int ch, uint32_t w, double sp, double sq, uint32_t st) {
-    MeshDev M{};
-    M.seg = seg;
-    M.ep_range = ep_range;
-    M.ep_ids = ep_ids;
-    M.cxy = cxy;
-    Ray r{ox, oy, dx, dy};
-    WalkState s;
-    s.kr = kr;
-    s.ch = ch;
-    s.w = w;
-    s.sp = sp;
-    s.sq = sq;
-    Term o;
-    o.st = st;
-    o.seg = walk_terminal(M, r, s, o.t, o.u, o.st);
-    return o;
 }
 
 // ---------------------------------------------------------------------------
