@@ -606,6 +606,7 @@ struct HistSm {
     unsigned int bins[MWT_HIST_LEN];
     unsigned long long steps_sum;
     unsigned long long warp_steps[32];  // per-warp partial step sums (owner-only updates)
+    unsigned warp_hm[32][2];            // per-warp hit / miss counts (owner-only updates)
 };
 
 __device__ __forceinline__ void hist_add_warp(HistSm *H, int seg, int steps, uint32_t st) {
@@ -617,9 +618,10 @@ __device__ __forceinline__ void hist_add_warp(HistSm *H, int seg, int steps, uin
     const unsigned ssum = __reduce_add_sync(m, (unsigned)(steps > 0 ? steps : 0));
     unsigned any = __reduce_or_sync(m, st) & 0xFFFu;
     if (lane == leader) {
-        if (hits) atomicAdd(H->bins + MWT_HIST_HIT, (unsigned)__popc(hits));
-        if (m & ~hits) atomicAdd(H->bins + MWT_HIST_MISS, (unsigned)__popc(m & ~hits));
-        H->warp_steps[threadIdx.x >> 5] += (unsigned long long)ssum;  // own slot: no atomic
+        const int w = threadIdx.x >> 5;  // this warp's own slots: no atomics
+        H->warp_hm[w][0] += (unsigned)__popc(hits);
+        H->warp_hm[w][1] += (unsigned)__popc(m & ~hits);
+        H->warp_steps[w] += (unsigned long long)ssum;
     }
     while (any) {
         const int b = __ffs(any) - 1;
@@ -759,7 +761,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
         for (int k = threadIdx.x; k < MWT_HIST_LEN; k += THREADS) H.bins[k] = 0u;
     if (threadIdx.x == 0) {
         H.steps_sum = 0ull;
-        for (int w = 0; w < 32; w++) H.warp_steps[w] = 0ull;
+        for (int w = 0; w < 32; w++) {
+            H.warp_steps[w] = 0ull;
+            H.warp_hm[w][0] = H.warp_hm[w][1] = 0u;
+        }
         s_next = (unsigned long long)cbeg;
     }
     __syncthreads();
@@ -888,6 +893,13 @@ __global__ void __launch_bounds__(THREADS, MINB)
             if (H.bins[k] && k != MWT_HIST_STEPS_SUM)
                 atomicAdd(reinterpret_cast<unsigned long long *>(hist + k), (unsigned long long)H.bins[k]);
         if (threadIdx.x == 0) {
+            unsigned long long hh = 0, mm = 0;
+            for (int w = 0; w < THREADS / 32; w++) {
+                hh += H.warp_hm[w][0];
+                mm += H.warp_hm[w][1];
+            }
+            if (hh) atomicAdd(reinterpret_cast<unsigned long long *>(hist + MWT_HIST_HIT), hh);
+            if (mm) atomicAdd(reinterpret_cast<unsigned long long *>(hist + MWT_HIST_MISS), mm);
             unsigned long long t = H.steps_sum;
             for (int w = 0; w < THREADS / 32; w++) t += H.warp_steps[w];
             if (t) atomicAdd(reinterpret_cast<unsigned long long *>(hist + MWT_HIST_STEPS_SUM), t);
