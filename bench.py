@@ -42,6 +42,16 @@ SEED = 0
 ALGO_BYTES_PER_STEP = 32  # 16-B link record + 16-B apex corner per triangle step
 
 
+def l2_peak():
+    """L2 read bandwidth measured on the box (profiles/r01_l2_peak.json,
+    tools/l2_peak.cu): the on-chip roof for meshes that live in L2."""
+    p = os.path.join(ROOT, "profiles", "r01_l2_peak.json")
+    if os.path.exists(p):
+        with open(p) as fh:
+            return float(json.load(fh)["l2_read_gbs"])
+    return None
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -328,7 +338,8 @@ def main():
                      "kernel": "k_trace (mwt_trace_generated_dev, box-entry launch)", "kernel_ms": kms,
                      "algo_bytes_per_launch": algo_bytes,
                      "algo_bytes_rule": "32 B per triangle step (one 32-B step record: 2 exit words + apex corner)",
-                     "peak_source": peak_src, "mesh_resident": "L2 (126 MB); HBM carries only per-ray output"},
+                     "peak_source": peak_src, "mesh_resident": "L2 (126 MB); HBM carries only per-ray output",
+                     "l2_peak": l2_peak(), "l2_frac": achieved / l2_peak() if l2_peak() else None},
         "histogram": {k: hsum[k] for k in ("rays", "hits", "misses", "steps_sum", "status")},
     }
 
