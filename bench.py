@@ -218,11 +218,19 @@ def main():
     from paper_2112_05570_b200 import _lib
     from paper_2112_05570_b200.engine import DeviceMesh, _stream, new_histogram, summarize_histogram
 
+    # functional check of the N > 1 code path on a one-GPU box only (never a
+    # measurement): MWT_BENCH_ONE_DEVICE=1 puts every rank on cuda:0 and uses gloo
+    one_dev = os.environ.get("MWT_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=dev)
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     box, parts = CONFIGS[args.config]
     mesh = DeviceMesh.from_files(*fixture(args.config, args.mesh), device=local)
     rays_per_gpu = sum(n for _, n in parts)
