@@ -717,7 +717,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
     k_trace(const __grid_constant__ MeshDev M, const __grid_constant__ Launch L, long long n,
             long long *hist, int refill_below) {
     __shared__ HistSm H;
-    __shared__ unsigned long long s_next;
+    __shared__ unsigned s_next;
     extern __shared__ __align__(16) unsigned char dsm[];
     const uint2 *srec = reinterpret_cast<const uint2 *>(dsm);
     const double2 *svxy = reinterpret_cast<const double2 *>(dsm + (SMEM ? M.crec_bytes : 0));
@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             H.warp_steps[w] = 0ull;
             H.warp_hm[w][0] = H.warp_hm[w][1] = 0u;
         }
-        s_next = (unsigned long long)cbeg;
+        s_next = 0u;
     }
     __syncthreads();
     HistSm *Hp = hist ? &H : nullptr;
@@ -773,13 +773,15 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
     const int lim = 4 * M.nt + 16;  // walk_step's guard
-    long long next = 0, end = 0;    // the warp's current grab
-    bool more = cbeg < cend;        // warp-uniform: the CTA range is not exhausted
+    // ray offsets within the CTA's range (32-bit: a range is < 2^32 rays)
+    const unsigned span = (unsigned)(cend > cbeg ? cend - cbeg : 0);
+    unsigned next = 0u, end = 0u;   // the warp's current grab
+    bool more = span > 0u;          // warp-uniform: the CTA range is not exhausted
 
     // lane phase: 0 idle, 1 walking, 2 reached its exit edge (epilogue pending),
     // 3 failed (TraversalError pending)
     int phase = 0;
-    long long idx = 0;
+    unsigned idx = 0u;
     Ray r{0.0, 0.0, 0.0, 0.0};
     WalkState s;
     s.kr = 0; s.ch = 0; s.steps = 0; s.w = 0; s.sp = 0.0; s.sq = 0.0; s.fast = false;
@@ -789,7 +791,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         unsigned walking = __ballot_sync(FULL, phase == 1);
         if (__popc(walking) <= refill_below) {
             if (phase >= 2) {
-                epilogue<!GEN>(&M, &L, Hp, sseg, idx, r.ox, r.oy, r.dx, r.dy, s.kr, s.ch, s.w, s.sp, s.sq, st,
+                epilogue<!GEN>(&M, &L, Hp, sseg, cbeg + (long long)idx, r.ox, r.oy, r.dx, r.dy, s.kr, s.ch, s.w, s.sp, s.sq, st,
                          s.steps, phase);
                 phase = 0;
             }
@@ -797,20 +799,20 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 const unsigned idle = ~walking;
                 const int nidle = __popc(idle), rank = __popc(idle & lt_mask);
                 // rays for the idle lanes: the rest of the current grab, then a new one
-                long long nb = end, ne = end;
+                unsigned nb = end, ne = end;
                 const int rem = (int)(end - next);
                 if (rem < nidle) {
-                    unsigned long long base = 0;
-                    if (lane == 0) base = atomicAdd(&s_next, (unsigned long long)kGrab);
+                    unsigned base = 0u;
+                    if (lane == 0) base = atomicAdd(&s_next, (unsigned)kGrab);
                     base = __shfl_sync(FULL, base, 0);
-                    nb = (long long)base;
-                    ne = nb + kGrab < cend ? nb + kGrab : cend;
-                    if (nb >= cend) nb = ne = cend;
+                    nb = base < span ? base : span;
+                    ne = span - nb > (unsigned)kGrab ? nb + kGrab : span;
                 }
                 if (phase == 0) {
-                    const long long i = rank < rem ? next + rank : nb + (rank - rem);
-                    if (rank < rem || i < ne) {
-                        idx = i;
+                    const unsigned o = rank < rem ? next + rank : nb + (rank - rem);
+                    if (rank < rem || o < ne) {
+                        idx = o;
+                        const long long i = cbeg + (long long)o;
                         const Init in = prologue_body<GEN>(M, btab, L.src, i);
                         if (!GEN && L.out.start) L.out.start[i] = in.start;
                         r.ox = in.ox; r.oy = in.oy; r.dx = in.dx; r.dy = in.dy;
@@ -827,7 +829,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 } else {
                     next = nb + (nidle - rem) < ne ? nb + (nidle - rem) : ne;
                     end = ne;
-                    more = next < end || ne < cend;
+                    more = next < end || ne < span;
                 }
             }
             walking = __ballot_sync(FULL, phase == 1);
