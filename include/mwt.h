@@ -92,8 +92,10 @@ int mwt_device_count(int *count);
  * (default 6) lanes of the warp still walk.  `variant` 2 (default) stages the
  * mesh's compact walk table in shared memory when it fits, one CTA per SM
  * whose size `min_blocks_per_sm` picks (3: 768 threads / 80 registers,
- * 4: 896 / 72 (default), 2: 1024 / 64), else walks the 32-B records from
- * global memory with the boundary table staged (896 threads); variant 1 always
+ * 4: 896 / 72 (default), 2: 1024 / 64), else the per-triangle compact table
+ * (16 B per triangle) when that fits, else walks the 32-B records from
+ * global memory with the boundary table staged (896 threads); variant 3 tries
+ * the per-triangle table first (A/B); variant 1 always
  * walks from global memory with 256-thread CTAs, `min_blocks_per_sm` CTAs per SM. */
 int mwt_set_tuning(int refill_below, int min_blocks_per_sm, int variant);
 

@@ -124,7 +124,7 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
                    Arena::align(P.ep_ids.size() * 4) + Arena::align(P.anchor.size() * 4) +
                    Arena::align(P.bu.size() * 8) + Arena::align(P.bpq.size() * 8) +
                    Arena::align(P.bword.size() * 4) + Arena::align(P.bbucket.size() * 4) +
-                   Arena::align(P.crec.size() * 4) +
+                   Arena::align(P.crec.size() * 4) + Arena::align(P.ctri.size() * 4) +
                    Arena::align((P.bu.size() + P.bpq.size()) * 8 + P.bword.size() * 4 + P.bbucket.size() * 4 + 64) +
                    Arena::align(P.vxy.size() * 8);
     Arena a;
@@ -147,6 +147,7 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     int32_t *bword = carve<int32_t>(a, P.bword.size());
     int32_t *bbucket = carve<int32_t>(a, P.bbucket.size());
     uint32_t *crec = carve<uint32_t>(a, P.crec.size());
+    uint32_t *ctri = carve<uint32_t>(a, P.ctri.size());
     double *vxy = carve<double>(a, P.vxy.size());
     // boundary blob: bu | bpq | bword | bbucket, each 16-B aligned
     auto a16 = [](size_t b) { return (b + 15) & ~(size_t)15; };
@@ -177,6 +178,7 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     up(bword, P.bword.data(), P.bword.size() * 4);
     up(bbucket, P.bbucket.data(), P.bbucket.size() * 4);
     up(crec, P.crec.data(), P.crec.size() * 4);
+    up(ctri, P.ctri.data(), P.ctri.size() * 4);
     up(vxy, P.vxy.data(), P.vxy.size() * 8);
     up(bblob, bblob_host.data(), bblob_bytes);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking);
@@ -211,6 +213,11 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
         m->dev.smem_bytes = sm + (int64_t)bblob_bytes <= mwt::kSmemWalkMax ? (int32_t)sm : 0;
         m->dev.seg_staged = m->dev.smem_bytes > 0 &&
                             sm + (int64_t)bblob_bytes + 32LL * P.ns <= mwt::kSmemWalkMax;
+        m->dev.ctri = reinterpret_cast<const uint4 *>(ctri);
+        const int64_t tm = 16LL * P.nt + 16LL * P.nv;
+        m->dev.tri_smem_bytes = tm + (int64_t)bblob_bytes <= mwt::kSmemWalkMax ? (int32_t)tm : 0;
+        m->dev.tri_seg_staged = m->dev.tri_smem_bytes > 0 &&
+                                tm + (int64_t)bblob_bytes + 32LL * P.ns <= mwt::kSmemWalkMax;
     }
     m->info.num_vertices = P.nv;
     m->info.num_triangles = P.nt;
@@ -220,7 +227,7 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
     m->info.device = device;
     m->info.device_bytes = (int64_t)bytes;
     m->info.walk_record_bytes = 32;
-    m->info.walk_smem_bytes = m->dev.smem_bytes;
+    m->info.walk_smem_bytes = m->dev.smem_bytes ? m->dev.smem_bytes : m->dev.tri_smem_bytes;
     *out = m;
     return MWT_OK;
 }

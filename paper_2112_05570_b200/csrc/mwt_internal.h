@@ -77,6 +77,7 @@ struct HostPacked {
     // compact walk table (shared-memory staged walk, see kCompact* below); empty
     // when the mesh exceeds the compact word limits
     std::vector<uint32_t> crec;     // 2 per record 3N+j (+ pad to 16 B)
+    std::vector<uint32_t> ctri;     // 4 per triangle: cw(edge i) | vid(corner i) << 18, i < 3; 0
     std::vector<double> vxy;        // 2 per vertex
 };
 
@@ -95,6 +96,12 @@ constexpr uint32_t kCOpen = 0x3FFFFu;
 constexpr uint32_t kCWordMask = 0x3FFFFu;
 constexpr int kCVidShift = 18;
 constexpr int kSmemWalkMax = 200 * 1024;  // staged only if the table fits this
+// Per-triangle compact table (meshes whose record table does not fit): 16 B
+// per triangle, word i = cw(edge i) | vid(corner i) << 18.  Entering N through
+// its edge j, the step reads word j (apex vid; its own edge word is the entry),
+// word (j+1)%3 and word (j+2)%3 -- the record 3N+j rebuilt from one 16-B load.
+// 16 B/tri + 16 B/vertex instead of 24 + 16: Hair-512 (7,986 triangles, 4,008
+// vertices) fits shared memory this way.
 
 // Build the packed layout; returns MWT_OK or an error code with *err set.
 int pack_mesh(const double *vx, const double *vy, int32_t nverts, const int32_t *tri_v,
@@ -137,6 +144,10 @@ struct MeshDev {
     int32_t bblob_bytes, bo_bpq, bo_bword, bo_bbucket;
     int32_t seg_staged;  // the segments (32 B each) also fit: staged after the blob
     int32_t gseg_staged;  // without the walk table: the segments fit after the blob
+    // per-triangle compact table (staged when the record table does not fit)
+    const uint4 *ctri;
+    int32_t tri_smem_bytes;  // 16 * nt + 16 * nv if that plus the blob fits kSmemWalkMax, else 0
+    int32_t tri_seg_staged;  // ... and the segments fit after it
 };
 
 struct BvhDev {

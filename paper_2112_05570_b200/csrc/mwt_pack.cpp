@@ -159,6 +159,10 @@ int pack_mesh(const double *vx, const double *vy, int32_t nv, const int32_t *tv,
                                 ((uint32_t)tv[3 * t + j] << kCVidShift);
                 P.crec[2 * k + 1] = cw((uint32_t)P.link[4LL * t + (j + 2) % 3]);
             }
+        P.ctri.assign(4LL * nt, 0u);
+        for (int t = 0; t < nt; t++)
+            for (int i = 0; i < 3; i++)
+                P.ctri[4LL * t + i] = cw((uint32_t)P.link[4LL * t + i]) | ((uint32_t)tv[3 * t + i] << kCVidShift);
         P.vxy.resize(2LL * nv);
         for (int v = 0; v < nv; v++) {
             P.vxy[2LL * v] = vx[v];

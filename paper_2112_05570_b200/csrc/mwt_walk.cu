@@ -712,7 +712,10 @@ __device__ __forceinline__ void bulk_stage(unsigned long long *bar, int n, void 
 // SMEM: the compact walk table (mwt_internal.h) is staged into shared memory
 // once per CTA and the tight loop reads it there (one CTA of THREADS per SM);
 // otherwise the tight loop reads the 32-B step records from global memory.
-template <bool GEN, int MINB, int THREADS, bool SMEM, bool STAGE = SMEM>
+// TRI (with SMEM): the per-triangle compact table is staged instead of the
+// per-record one (meshes too large for the latter); locate and the
+// first-triangle words then read global memory.
+template <bool GEN, int MINB, int THREADS, bool SMEM, bool STAGE = SMEM, bool TRI = false>
 __global__ void __launch_bounds__(THREADS, MINB)
     k_trace(const __grid_constant__ MeshDev M, const __grid_constant__ Launch L, long long n,
             long long *hist, int refill_below) {
@@ -720,12 +723,14 @@ __global__ void __launch_bounds__(THREADS, MINB)
     __shared__ unsigned s_next;
     extern __shared__ __align__(16) unsigned char dsm[];
     const uint2 *srec = reinterpret_cast<const uint2 *>(dsm);
-    const double2 *svxy = reinterpret_cast<const double2 *>(dsm + (SMEM ? M.crec_bytes : 0));
+    const uint4 *stri = reinterpret_cast<const uint4 *>(dsm);
+    const int tbytes = !SMEM ? 0 : TRI ? 16 * M.nt : M.crec_bytes;  // the table; vxy follows
+    const double2 *svxy = reinterpret_cast<const double2 *>(dsm + tbytes);
     __shared__ MeshDev::BSide sbs[4];
     if (threadIdx.x < 4) sbs[threadIdx.x] = M.bs[threadIdx.x];
     BTab btab{M.bu, M.bpq, M.bword, M.bbucket, sbs, nullptr, nullptr};
     const double4 *sseg = nullptr;
-    const int wbytes = SMEM ? M.smem_bytes : 0;  // the walk table, then the boundary blob, segments
+    const int wbytes = !SMEM ? 0 : TRI ? M.tri_smem_bytes : M.smem_bytes;  // the walk table, then the boundary blob, segments
     if (SMEM || STAGE) {
         __shared__ __align__(8) unsigned long long stage_bar;
         void *dst[4];
@@ -733,11 +738,14 @@ __global__ void __launch_bounds__(THREADS, MINB)
         unsigned bytes[4];
         int np = 0;
         if (SMEM) {
-            dst[np] = dsm; src[np] = M.crec; bytes[np++] = (unsigned)M.crec_bytes;
-            dst[np] = dsm + M.crec_bytes; src[np] = M.vxy;
-            bytes[np++] = (unsigned)(M.smem_bytes - M.crec_bytes);
-            btab.srec = srec;
-            btab.svxy = svxy;
+            dst[np] = dsm; src[np] = TRI ? (const void *)M.ctri : (const void *)M.crec;
+            bytes[np++] = (unsigned)tbytes;
+            dst[np] = dsm + tbytes; src[np] = M.vxy;
+            bytes[np++] = (unsigned)(wbytes - tbytes);
+            if (!TRI) {
+                btab.srec = srec;
+                btab.svxy = svxy;
+            }
         }
         if (STAGE) {
             const unsigned char *bb = dsm + wbytes;
@@ -746,7 +754,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             btab.bpq = reinterpret_cast<const double4 *>(bb + M.bo_bpq);
             btab.bword = reinterpret_cast<const int32_t *>(bb + M.bo_bword);
             btab.bbucket = reinterpret_cast<const int32_t *>(bb + M.bo_bbucket);
-            if (SMEM ? M.seg_staged : M.gseg_staged) {
+            if (SMEM ? (TRI ? M.tri_seg_staged : M.seg_staged) : M.gseg_staged) {
                 dst[np] = dsm + wbytes + M.bblob_bytes; src[np] = M.seg;
                 bytes[np++] = 32u * (unsigned)M.ns;
                 sseg = reinterpret_cast<const double4 *>(dsm + wbytes + M.bblob_bytes);
@@ -854,7 +862,19 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     const uint32_t k = fl ? s.w : 0u;
                     uint32_t wx, wy;
                     double2 A;
-                    if (SMEM) {
+                    if (SMEM && TRI) {
+                        // record 3N + j from triangle N's 16-B entry: apex = corner j,
+                        // exits = edges (j+1)%3, (j+2)%3
+                        const uint32_t N = __umulhi(k, 0xAAAAAAABu) >> 1;
+                        const uint32_t j = k - 3u * N;
+                        const uint4 X = stri[N];
+                        const uint32_t a = j == 0u ? X.x : (j == 1u ? X.y : X.z);
+                        const uint32_t b = j == 0u ? X.y : (j == 1u ? X.z : X.x);
+                        const uint32_t c = j == 0u ? X.z : (j == 1u ? X.x : X.y);
+                        A = svxy[a >> kCVidShift];
+                        wx = b & kCWordMask;
+                        wy = c & kCWordMask;
+                    } else if (SMEM) {
                         const uint2 X = srec[k];
                         A = svxy[X.x >> kCVidShift];
                         wx = X.x & kCWordMask;
@@ -956,7 +976,7 @@ __global__ void __launch_bounds__(kThreads) k_histogram(const int32_t *seg, cons
 
 static int g_refill_below = 6;  // tuned on B200 (tools/breakdown.py): refill when <= 6 lanes still walk
 static int g_min_blocks = 4;    // register budget; see launch_k_trace_any
-static int g_variant = 2;       // 2: shared-memory staged walk when the compact table fits, else 1
+static int g_variant = 2;       // 2: shared-memory staged walk when a compact table fits, else 1; 3: per-triangle table first
 
 // the launch-configuration caches below are process-wide: calls from several
 // host threads (one per device or stream) serialise on this lock
@@ -993,13 +1013,14 @@ static int persistent_grid(K kernel, long long n, int threads = kThreads, int sm
 }
 
 
-template <bool GEN, int MINB, int THREADS, bool SMEM, bool STAGE = SMEM>
+template <bool GEN, int MINB, int THREADS, bool SMEM, bool STAGE = SMEM, bool TRI = false>
 static bool launch_k_trace(const MeshDev &m, const Launch &L, long long n, long long *hist,
                            void *stream) {
-    auto kern = k_trace<GEN, MINB, THREADS, SMEM, STAGE>;
-    const int dyn = SMEM ? m.smem_bytes + m.bblob_bytes + (m.seg_staged ? 32 * m.ns : 0)
+    auto kern = k_trace<GEN, MINB, THREADS, SMEM, STAGE, TRI>;
+    const int dyn = SMEM && TRI ? m.tri_smem_bytes + m.bblob_bytes + (m.tri_seg_staged ? 32 * m.ns : 0)
+                  : SMEM  ? m.smem_bytes + m.bblob_bytes + (m.seg_staged ? 32 * m.ns : 0)
                   : STAGE ? m.bblob_bytes + (m.gseg_staged ? 32 * m.ns : 0) : 0;
-    if (SMEM && m.smem_bytes <= 0) return false;  // the walk table does not fit: variant 1
+    if (SMEM && (TRI ? m.tri_smem_bytes : m.smem_bytes) <= 0) return false;  // does not fit
     if (STAGE) {
         int dev = 0;
         cudaGetDevice(&dev);
@@ -1026,14 +1047,18 @@ static void launch_k_trace_any(const MeshDev &m, const Launch &L, long long n, l
     // shared-memory walk table: one CTA per SM; min_blocks picks its size
     // (3: 768 threads / 80 registers, 4: 896 / 72 (default, measured best),
     // 2: 1024 / 64)
-    if (g_variant == 2) {
+    if (g_variant == 3 && launch_k_trace<GEN, 1, 896, true, true, true>(m, L, n, hist, stream))
+        return;  // (A/B knob: the per-triangle table even where the record table fits)
+    if (g_variant >= 2) {
         const bool ok = g_min_blocks == 3   ? launch_k_trace<GEN, 1, 768, true>(m, L, n, hist, stream)
                         : g_min_blocks == 2 ? launch_k_trace<GEN, 1, 1024, true>(m, L, n, hist, stream)
                                             : launch_k_trace<GEN, 1, 896, true>(m, L, n, hist, stream);
         if (ok) return;
     }
+    // the per-triangle compact table when the record table does not fit
+    if (g_variant >= 2 && launch_k_trace<GEN, 1, 896, true, true, true>(m, L, n, hist, stream)) return;
     // global walk records; boundary table (and segments when they fit) staged
-    if (g_variant == 2 && launch_k_trace<GEN, 1, 896, false, true>(m, L, n, hist, stream)) return;
+    if (g_variant >= 2 && launch_k_trace<GEN, 1, 896, false, true>(m, L, n, hist, stream)) return;
     if (g_min_blocks == 3)
         launch_k_trace<GEN, 3, kThreads, false>(m, L, n, hist, stream);
     else if (g_min_blocks == 2)
@@ -1094,7 +1119,7 @@ int launch_histogram(const int32_t *seg, const int32_t *steps, const uint32_t *s
 void set_tuning(int refill_below, int min_blocks, int variant) {
     if (refill_below >= 0) g_refill_below = refill_below > 31 ? 31 : refill_below;
     if (min_blocks >= 2 && min_blocks <= 4) g_min_blocks = min_blocks;
-    if (variant == 1 || variant == 2) g_variant = variant;
+    if (variant >= 1 && variant <= 3) g_variant = variant;
 }
 
 }  // namespace mwt

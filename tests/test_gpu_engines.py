@@ -74,11 +74,12 @@ def test_locate_matches_oracle_everywhere():
         assert np.array_equal(gst & 128, rst & 128)  # tie flag
 
 
-def test_generated_kernel_equals_explicit_rays_and_histogram():
+@pytest.mark.parametrize("cfg", ["lines1024", "hair512"])  # record table / per-triangle table
+def test_generated_kernel_equals_explicit_rays_and_histogram(cfg):
     import torch
     from paper_2112_05570_b200.engine import DeviceMesh, new_histogram
     from paper_2112_05570_b200.sharding import histogram_host
-    paths = fixture_paths("lines1024", "mwt") or fixture_paths("lines1024", "cdt")
+    paths = fixture_paths(cfg, "mwt") or fixture_paths(cfg, "cdt")
     m = DeviceMesh.from_files(*paths)
     n = 1 << 18
     for mode in (0, 1):
@@ -102,18 +103,22 @@ def test_generated_kernel_equals_explicit_rays_and_histogram():
         assert np.array_equal(h2.cpu().numpy(), ref)
 
 
-@pytest.mark.parametrize("cfg,refill,minb,variant", [
-    ("hair512", 0, 4, 1), ("hair512", 4, 3, 1), ("hair512", 16, 2, 1), ("hair512", 31, 4, 1),
-    ("hair512", 4, 4, 2),  # table too large for shared memory: falls back to variant 1
-    ("lines1024", 0, 4, 2), ("lines1024", 4, 4, 2), ("lines1024", 31, 4, 2), ("lines1024", 4, 4, 1),
-    ("lines1024", 6, 3, 2), ("lines1024", 6, 2, 2), ("floorplan64", 6, 4, 2)])
-def test_tuning_knobs_do_not_change_results(cfg, refill, minb, variant):
+@pytest.mark.parametrize("cfg,refill,minb,variant,mode", [
+    ("hair512", 0, 4, 1, 0), ("hair512", 4, 3, 1, 0), ("hair512", 16, 2, 1, 0), ("hair512", 31, 4, 1, 0),
+    # record table too large for shared memory: the per-triangle table is staged
+    ("hair512", 4, 4, 2, 0), ("hair512", 6, 4, 2, 1), ("hair512", 0, 4, 3, 0),
+    # variant 3: the per-triangle table where the record table also fits
+    ("lines1024", 6, 4, 3, 0), ("lines1024", 6, 4, 3, 1), ("lines64", 31, 4, 3, 0),
+    ("lines1024", 0, 4, 2, 0), ("lines1024", 4, 4, 2, 0), ("lines1024", 31, 4, 2, 0), ("lines1024", 4, 4, 1, 0),
+    ("lines1024", 6, 3, 2, 0), ("lines1024", 6, 2, 2, 0), ("floorplan64", 6, 4, 2, 0),
+    ("grass4096", 6, 4, 2, 0), ("grass4096", 6, 4, 3, 1)])  # neither table fits: global records
+def test_tuning_knobs_do_not_change_results(cfg, refill, minb, variant, mode):
     from oracle import oracle as orc
     from paper_2112_05570_b200 import _lib
     from paper_2112_05570_b200.engine import DeviceMesh
     paths = fixture_paths(cfg, "mwt")
     m, om = DeviceMesh.from_files(*paths), orc.Mesh.from_files(*paths)
-    rays = orc.raygen(0, (0, 0, 1, 1), 2, 0, 50000)
+    rays = orc.raygen(mode, (0, 0, 1, 1), 2, 0, 50000)
     ref = om.trace(rays)
     _lib.check(_lib.lib.mwt_set_tuning(refill, minb, variant))
     try:
