@@ -211,7 +211,8 @@ __device__ __forceinline__ int locate(const MeshDev &M, double px, double py, ui
 
 // ---------------------------------------------------------------------------
 // K4: the walk, accel.py:138-213.  State between steps: current triangle,
-// the chosen exit edge word w and the side values (sp, sq) of its endpoints.
+// the chosen exit edge word w and whether its endpoints' sides are strict
+// (sp < 0 < sq; the values themselves are recomputed where needed).
 // Entering neighbour N across w through N's edge j, the two shared corners
 // keep their side values (accel.py:153-159 caches them per vertex), so one
 // step loads link[N] (16 B) and the apex corner cxy[3N + j] (16 B) -- both
@@ -223,10 +224,17 @@ __device__ __forceinline__ int locate(const MeshDev &M, double px, double py, ui
 // triangle (kr) and which candidate it exits through (ch: 0 = edge (j+1)%3,
 // 1 = edge (j+2)%3); the triangle id and exit edge are only needed at the
 // exit, and are recovered there (cur = kr / 3, ei = (kr % 3 + 1 + ch) % 3).
+// The side values (sp, sq) of the chosen exit edge's endpoints decide the
+// state (fast: sp < 0 < sq) but are not carried between steps: a step in the
+// fast state never reads them, and the rare consumers (the general rule, the
+// grazing fallback) recompute them from the edge's corners -- side_of is a
+// pure function of the vertex, so the value is the reference's cached one
+// (accel.py:153-159).  That keeps four registers and four selects per step
+// out of the walk loop.
 struct WalkState {
     int kr, ch, steps;
     uint32_t w;     // word of the exit edge just chosen
-    double sp, sq;  // side values of that edge's endpoints, corners (ei+1)%3, (ei+2)%3
+    double sp, sq;  // (walk_first / boundary_start only) sides of corners (ei+1)%3, (ei+2)%3
     bool fast;      // sp < 0 < sq: the next step may take the one-candidate fast path
 };
 
@@ -349,35 +357,24 @@ __device__ __forceinline__ bool walk_step(const MeshDev &M, const Ray &r, WalkSt
     const double c = side_of(r, A);
     s.kr = (int)k;
     if (s.fast && c != 0.0) {
-        // (sp, sq) of the new exit: E1 -> (sp, c), E2 -> (c, sq)
-        if (c > 0.0) {
-            s.sq = c;
-            s.w = (uint32_t)W.x;
-            s.ch = 0;
-        } else {
-            s.sp = c;
-            s.w = (uint32_t)W.y;
-            s.ch = 1;
-        }
+        // E1 -> (sp, c), E2 -> (c, sq): still sp < 0 < sq
+        s.w = (uint32_t)(c > 0.0 ? W.x : W.y);
+        s.ch = c > 0.0 ? 0 : 1;
         return true;
     }
-    const int j = (int)(k % 3u);
-    const double a = s.sq, b = s.sp;
+    // the shared corners' sides, recomputed: a = corner (j+1)%3 (the previous
+    // exit's sq), b = corner (j+2)%3 (its sp)
+    const int j = (int)(k % 3u), N = (int)(k / 3u);
+    const double a = side_of(r, __ldg(M.cxy + 3 * N + (j + 1) % 3));
+    const double b = side_of(r, __ldg(M.cxy + 3 * N + (j + 2) % 3));
     const uint32_t g = walk_general(j, a, b, c, st);
     st = g & 0xFFFFFu;
     const int sel = (int)(g >> 20) - 1;
     if (sel < 0) return false;
-    if (sel == 0) {  // E1
-        s.sp = b;
-        s.sq = c;
-        s.w = (uint32_t)W.x;
-    } else {  // E2
-        s.sp = c;
-        s.sq = a;
-        s.w = (uint32_t)W.y;
-    }
+    const double sp = sel == 0 ? b : c, sq = sel == 0 ? c : a;  // E1: (b, c); E2: (c, a)
+    s.w = (uint32_t)(sel == 0 ? W.x : W.y);
     s.ch = sel;
-    s.fast = s.sp < 0.0 && 0.0 < s.sq;
+    s.fast = sp < 0.0 && 0.0 < sq;
     return true;
 }
 
@@ -402,7 +399,8 @@ __device__ __forceinline__ int walk_terminal(const MeshDev &M, const Ray &r, con
         const int ei = (j + 1 + s.ch) % 3;
         const double2 pa = __ldg(M.cxy + 3 * cur + (ei + 1) % 3);
         const double2 pb = __ldg(M.cxy + 3 * cur + (ei + 2) % 3);
-        const double wq = s.sp != s.sq ? s.sp / (s.sp - s.sq) : 0.5;
+        const double sp = side_of(r, pa), sq = side_of(r, pb);  // the exit edge's sides
+        const double wq = sp != sq ? sp / (sp - sq) : 0.5;
         const double x = pa.x + wq * (pb.x - pa.x);
         const double y = pa.y + wq * (pb.y - pa.y);
         t = (x - r.ox) * r.dx + (y - r.oy) * r.dy;
@@ -471,7 +469,7 @@ struct Launch {
 
 // Per-ray prologue result (raygen or load, locate, first triangle)
 struct Init {
-    double ox, oy, dx, dy, sp, sq;
+    double ox, oy, dx, dy;
     uint32_t w, st;
     int cur, ei, steps, phase, start;
     bool fast;
@@ -562,7 +560,7 @@ __device__ __forceinline__ Init prologue_body(const MeshDev &M, const BTab &T, c
         WalkState bs;
         if (boundary_start(M, T, r, bs)) {
             o.start = bs.kr / 3;
-            o.sp = bs.sp; o.sq = bs.sq; o.w = bs.w; o.cur = bs.kr; o.ei = bs.ch; o.steps = 0;
+            o.w = bs.w; o.cur = bs.kr; o.ei = bs.ch; o.steps = 0;
             o.fast = true;
             o.phase = 1;
             o.st = MWT_ST_BOUNDARY;
@@ -595,7 +593,7 @@ __device__ __forceinline__ Init prologue_body(const MeshDev &M, const BTab &T, c
     } else {
         o.phase = (s.w & kStopBit) ? 2 : 1;
     }
-    o.sp = s.sp; o.sq = s.sq; o.w = s.w; o.cur = s.kr; o.ei = s.ch; o.steps = s.steps;
+    o.w = s.w; o.cur = s.kr; o.ei = s.ch; o.steps = s.steps;
     o.fast = s.fast;
     return o;
 }
@@ -636,7 +634,7 @@ __device__ __forceinline__ void hist_add_warp(HistSm *H, int seg, int steps, uin
 template <bool END>
 __device__ __forceinline__ void epilogue(const MeshDev *__restrict__ Mg, const Launch *__restrict__ L,
                                       HistSm *H, const double4 *sseg, long long i, double ox, double oy, double dx,
-                                      double dy, int kr, int ch, uint32_t w, double sp, double sq,
+                                      double dy, int kr, int ch, uint32_t w,
                                       uint32_t st, int steps, int phase) {
     int seg = -1;
     double t = CUDART_NAN, u = CUDART_NAN;
@@ -646,8 +644,6 @@ __device__ __forceinline__ void epilogue(const MeshDev *__restrict__ Mg, const L
         s.kr = kr;
         s.ch = ch;
         s.w = w;
-        s.sp = sp;
-        s.sq = sq;
         seg = walk_terminal(*Mg, r, s, t, u, st, sseg);
     }
     const TraceOut &O = L->out;
@@ -792,14 +788,14 @@ __global__ void __launch_bounds__(THREADS, MINB)
     unsigned idx = 0u;
     Ray r{0.0, 0.0, 0.0, 0.0};
     WalkState s;
-    s.kr = 0; s.ch = 0; s.steps = 0; s.w = 0; s.sp = 0.0; s.sq = 0.0; s.fast = false;
+    s.kr = 0; s.ch = 0; s.steps = 0; s.w = 0; s.fast = false;
     uint32_t st = 0;
 
     while (true) {
         unsigned walking = __ballot_sync(FULL, phase == 1);
         if (__popc(walking) <= refill_below) {
             if (phase >= 2) {
-                epilogue<!GEN>(&M, &L, Hp, sseg, cbeg + (long long)idx, r.ox, r.oy, r.dx, r.dy, s.kr, s.ch, s.w, s.sp, s.sq, st,
+                epilogue<!GEN>(&M, &L, Hp, sseg, cbeg + (long long)idx, r.ox, r.oy, r.dx, r.dy, s.kr, s.ch, s.w, st,
                          s.steps, phase);
                 phase = 0;
             }
@@ -824,7 +820,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
                         const Init in = prologue_body<GEN>(M, btab, L.src, i);
                         if (!GEN && L.out.start) L.out.start[i] = in.start;
                         r.ox = in.ox; r.oy = in.oy; r.dx = in.dx; r.dy = in.dy;
-                        s.sp = in.sp; s.sq = in.sq; s.w = in.w; s.kr = in.cur;
+                        s.w = in.w; s.kr = in.cur;
                         st = in.st;
                         phase = in.phase;
                         s.fast = in.fast;
@@ -890,8 +886,6 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     const uint32_t nw = pos ? wx : wy;
                     s.steps += ok ? 1 : 0;
                     s.kr = ok ? (int)k : s.kr;
-                    s.sq = (ok && pos) ? c : s.sq;
-                    s.sp = (ok && !pos) ? c : s.sp;
                     s.ch = ok ? (pos ? 0 : 1) : s.ch;
                     s.w = ok ? nw : s.w;
                     const bool stop = ok && (nw & (SMEM ? kCStop : kStopBit));
