@@ -847,7 +847,12 @@ __global__ void __launch_bounds__(THREADS, MINB)
         // once the range is exhausted, until none remains.  A lane leaves on a
         // zero apex side (the general rule decides that step), at its stop
         // edge, or at the step guard (walk_step below flags the error).
-        bool fl = phase == 1 && s.fast && s.steps < lim;
+        // The guard is checked once per group of 5 steps (a lane enters a
+        // group only with steps < lim - 5, so no step in it passes the guard;
+        // the last few steps before the guard run in walk_step), and the stop
+        // edge ends the lane's walk in the loop but its phase is set after it.
+        const int glim = lim - 5;
+        bool fl = phase == 1 && s.fast && s.steps < glim;
         {
             const int thr = more ? refill_below : 0;
             while (__popc(__ballot_sync(FULL, fl)) > thr) {
@@ -888,12 +893,13 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     s.kr = ok ? (int)k : s.kr;
                     s.ch = ok ? (pos ? 0 : 1) : s.ch;
                     s.w = ok ? nw : s.w;
-                    const bool stop = ok && (nw & (SMEM ? kCStop : kStopBit));
-                    phase = stop ? 2 : phase;
-                    fl = ok && !stop && s.steps < lim;
+                    fl = ok && !(nw & (SMEM ? kCStop : kStopBit));
                 }
+                fl = fl && s.steps < glim;
             }
         }
+        // a phase-1 lane holds a stop word only if the loop just reached it
+        if (phase == 1 && (s.w & (SMEM ? (kStopBit | kCStop) : kStopBit))) phase = 2;
         if (SMEM && (s.w & (kStopBit | kCStop)) == kCStop) s.w = expand_cword(s.w);
         // one full-rule step for every lane that left the tight loop still
         // walking (zero side, the general state, the guard); lanes it merely
