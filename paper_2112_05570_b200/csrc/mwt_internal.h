@@ -47,6 +47,9 @@ constexpr uint32_t kStopBit = 0x80000000u;
 constexpr uint32_t kBoundaryBit = 0x40000000u;
 constexpr uint32_t kOpenWord = 0xFFFFFFFFu;
 constexpr uint32_t kSidMask = 0x3FFFFFFFu;
+// boundary-edge word flag: the edge's endpoints are off the side line, so the
+// start test is evaluated on the device (bu then holds the edge's extent)
+constexpr uint32_t kBExact = 0x80000000u;
 
 struct HostPacked {
     int32_t nv = 0, nt = 0, ns = 0;
@@ -70,9 +73,9 @@ struct HostPacked {
         int32_t boff, nb;  // its buckets
         double scale;      // nb / (hi - lo)
     } sides[4];
-    std::vector<double> bu;         // 2 per edge: umin, umax
+    std::vector<double> bu;         // 2 per edge: the open start interval (see mwt_pack.cpp)
     std::vector<double> bpq;        // 4 per edge: P (corner (j+1)%3), Q (corner (j+2)%3)
-    std::vector<int32_t> bword;     // (T << 2) | j, j = the boundary edge's index in T
+    std::vector<int32_t> bword;     // 3T + j, j = the boundary edge's index in T (| kBExact)
     std::vector<int32_t> bbucket;   // first edge (side-local) whose umax > bucket start
     // compact walk table (shared-memory staged walk, see kCompact* below); empty
     // when the mesh exceeds the compact word limits
@@ -129,7 +132,7 @@ struct MeshDev {
         int32_t axis, off, cnt, boff, nb;
         double c, lo, hi, scale;
     } bs[4];
-    const double2 *bu;      // (umin, umax) per edge
+    const double2 *bu;      // the open start interval per edge (mwt_pack.cpp start_interval)
     const double4 *bpq;     // (P.x, P.y, Q.x, Q.y) per edge
     const int32_t *bword;
     const int32_t *bbucket;

@@ -24,6 +24,68 @@ inline double sa2(double ax, double ay, double bx, double by, double cx, double 
     return (bx - ax) * (cy - ay) - (by - ay) * (cx - ax);
 }
 
+// Doubles in a totally ordered integer key (-0.0 and +0.0 share key 0).
+inline int64_t dkey(double x) {
+    int64_t b;
+    std::memcpy(&b, &x, 8);
+    return b >= 0 ? b : INT64_MIN - b;
+}
+inline double dval(int64_t k) {
+    const int64_t b = k >= 0 ? k : INT64_MIN - k;
+    double x;
+    std::memcpy(&x, &b, 8);
+    return x;
+}
+
+// The box-entry start test (device boundary_start) for an origin o strictly
+// inside boundary edge PQ of triangle T (apex A) on the side line:
+//   _contains (accel.py:219-223): ej = sa2(P, Q, o) >= -1e-15 and the flood
+//   bound (accel.py:226-238) on the other two: e1 = sa2(Q, A, o) > 1e-12,
+//   e2 = sa2(A, P, o) > 1e-12.
+// When P and Q lie exactly on the side line (coordinate c), o = (u, c) or
+// (c, u) makes ej = +-0 and reduces e1, e2 to a constant combined with ONE
+// rounded product of a rounded difference in u -- each a monotone function of
+// u under IEEE rounding.  So the test holds exactly on one interval of
+// doubles, found here by bisection with the device's own expressions; the
+// kernel then compares u against its bounds instead of evaluating the test.
+// Returns the open interval (L, H) (L >= H: empty).
+struct OpenIv {
+    double lo, hi;
+};
+OpenIv start_interval(int axis, double c, double umin, double umax, double px, double py, double qx,
+                      double qy, double ax, double ay) {
+    auto at = [&](int64_t k, int which) {
+        const double u = dval(k);
+        const double ox = axis == 0 ? u : c, oy = axis == 0 ? c : u;
+        if (which == 0) return sa2(qx, qy, ax, ay, ox, oy) > 1e-12;
+        if (which == 1) return sa2(ax, ay, px, py, ox, oy) > 1e-12;
+        return sa2(px, py, qx, qy, ox, oy) >= -1e-15;
+    };
+    int64_t lo = dkey(umin) + 1, hi = dkey(umax) - 1;  // the doubles strictly inside
+    if (lo > hi) return {umax, umax};
+    for (int which = 0; which < 3; which++) {
+        const bool fl = at(lo, which), fh = at(hi, which);
+        if (fl && fh) continue;
+        if (!fl && !fh) return {umax, umax};
+        int64_t a = lo, b = hi;  // monotone: bisect for the switch point
+        if (!fl) {  // false ... true: smallest true
+            while (a + 1 < b) {
+                const int64_t m = a + (b - a) / 2;
+                (at(m, which) ? b : a) = m;
+            }
+            lo = b;
+        } else {  // true ... false: largest true
+            while (a + 1 < b) {
+                const int64_t m = a + (b - a) / 2;
+                (at(m, which) ? a : b) = m;
+            }
+            hi = a;
+        }
+        if (lo > hi) return {umax, umax};
+    }
+    return {dval(lo - 1), dval(hi + 1)};
+}
+
 struct Ctx {
     const double *vx, *vy;
     const int32_t *tv, *tn;
@@ -221,6 +283,7 @@ int pack_mesh(const double *vx, const double *vy, int32_t nv, const int32_t *tv,
         struct E {
             double umin, umax, px, py, qx, qy;
             int32_t word;
+            double ax, ay;  // apex (corner opposite the edge)
         };
         std::vector<E> es;
         bool ok = true;
@@ -232,8 +295,9 @@ int pack_mesh(const double *vx, const double *vy, int32_t nv, const int32_t *tv,
                 // boundary edges at points within its tolerance); the device
                 // tests containment with the actual coordinates
                 const double ua = axis == 0 ? vx[a] : vy[a], ub = axis == 0 ? vx[b] : vy[b];
+                const int ap = tv[3 * t + i];
                 es.push_back({std::min(ua, ub), std::max(ua, ub), vx[a], vy[a], vx[b], vy[b],
-                              (int32_t)(3 * t + i)});
+                              (int32_t)(3 * t + i), vx[ap], vy[ap]});
             }
         if (!ok || es.empty()) continue;
         std::sort(es.begin(), es.end(), [](const E &p, const E &q) { return p.umin < q.umin; });
@@ -252,13 +316,20 @@ int pack_mesh(const double *vx, const double *vy, int32_t nv, const int32_t *tv,
         S.scale = S.nb / (S.hi - S.lo);
         S.boff = (int32_t)P.bbucket.size();
         for (const E &e : es) {
-            P.bu.push_back(e.umin);
-            P.bu.push_back(e.umax);
+            // bu: the exact start interval when P and Q lie on the side line,
+            // else the edge's extent with kBExact set on the word (the
+            // kernel then evaluates the test itself)
+            const bool online = axis == 0 ? (e.py == S.c && e.qy == S.c) : (e.px == S.c && e.qx == S.c);
+            const OpenIv iv = online ? start_interval(axis, S.c, e.umin, e.umax, e.px, e.py, e.qx, e.qy,
+                                                      e.ax, e.ay)
+                                     : OpenIv{e.umin, e.umax};
+            P.bu.push_back(iv.lo);
+            P.bu.push_back(iv.hi);
             P.bpq.push_back(e.px);
             P.bpq.push_back(e.py);
             P.bpq.push_back(e.qx);
             P.bpq.push_back(e.qy);
-            P.bword.push_back(e.word);
+            P.bword.push_back(online ? e.word : (int32_t)((uint32_t)e.word | kBExact));
         }
         int k = 0;
         for (int b = 0; b < S.nb; b++) {

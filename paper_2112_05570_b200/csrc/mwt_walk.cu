@@ -511,19 +511,26 @@ __device__ __forceinline__ bool boundary_start(const MeshDev &M, const BTab &T, 
     int b = (int)((u - S.lo) * S.scale);
     b = b < 0 ? 0 : (b >= S.nb ? S.nb - 1 : b);
     int e = T.bbucket[S.boff + b];
+    // bu holds each edge's exact start interval (mwt_pack.cpp): u inside it
+    // <=> strictly inside the edge and the _contains / flood-bound test holds;
+    // a u past it moves on, and then fails the next edge's lower bound
     double2 U = T.bu[S.off + e];
     while (ok && u >= U.y && e < S.cnt - 1) U = T.bu[S.off + (++e)];
-    ok = ok && U.x < u && u < U.y;  // strictly inside the edge (on a vertex: general path)
+    ok = ok && U.x < u && u < U.y;
     const double4 PQ = T.bpq[S.off + e];
-    const uint32_t word = (uint32_t)T.bword[S.off + e];
+    uint32_t word = (uint32_t)T.bword[S.off + e];
     const double2 P = make_double2(PQ.x, PQ.y), Q = make_double2(PQ.z, PQ.w);
-    const double2 A = __ldg(M.cxy + word);  // apex corner j of T: cxy[3T + j], word = 3T + j
-    // _contains values in the reference's form: edge i -> (corner i+1, corner i+2)
-    const double ej = sa2(P, Q, r.ox, r.oy);
-    const double e1 = sa2(Q, A, r.ox, r.oy);
-    const double e2 = sa2(A, P, r.ox, r.oy);
+    if (word & kBExact) {  // endpoints off the side line: the test in full (rare)
+        word &= ~kBExact;
+        const double2 A = __ldg(M.cxy + word);  // apex corner j of T: cxy[3T + j], word = 3T + j
+        // _contains values in the reference's form: edge i -> (corner i+1, corner i+2)
+        const double ej = sa2(P, Q, r.ox, r.oy);
+        const double e1 = sa2(Q, A, r.ox, r.oy);
+        const double e2 = sa2(A, P, r.ox, r.oy);
+        ok = ok && ej >= -1e-15 && e1 > 1e-12 && e2 > 1e-12;
+    }
     const double sa = side_of(r, P), sb = side_of(r, Q);
-    ok = ok && ej >= -1e-15 && e1 > 1e-12 && e2 > 1e-12 && sb < 0.0 && 0.0 < sa;
+    ok = ok && sb < 0.0 && 0.0 < sa;
     if (ok) {
         s.w = word;
         s.sq = sa;  // side of corner (j+1)%3

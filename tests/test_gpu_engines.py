@@ -1,6 +1,7 @@
 """Device engines against the oracle at scale, the drop-in API, histograms,
 edge cases and full-size properties."""
 import os
+import struct
 
 import numpy as np
 import pytest
@@ -277,3 +278,68 @@ def test_chained_secondary_rays():
             assert np.array_equal(got2[k], ref2[k]), (cfg, "secondary", k)
         h2 = ref2["seg"] >= 0
         assert np.array_equal(got2["t"][h2], ref2["t"][h2])
+
+
+def _dkey(x):
+    b = struct.unpack("<q", struct.pack("<d", x))[0]
+    return b if b >= 0 else -(1 << 63) - b
+
+
+def _dval(k):
+    b = k if k >= 0 else -(1 << 63) - k
+    return struct.unpack("<d", struct.pack("<q", b))[0]
+
+
+def _sa2(a, b, p):  # geometry.py:81-83, CPython floats (binary64, no FMA)
+    return (b[0] - a[0]) * (p[1] - a[1]) - (b[1] - a[1]) * (p[0] - a[0])
+
+
+def _switch(f, lo, hi):
+    """Key of the first double in [lo, hi] where the monotone predicate f flips."""
+    a, b = lo, hi
+    fa = f(a)
+    while a + 1 < b:
+        m = (a + b) // 2
+        if f(m) == fa:
+            a = m
+        else:
+            b = m
+    return b
+
+
+@pytest.mark.parametrize("cfg", ["lines64", "lines1024"])
+def test_box_entry_start_at_interval_bounds(cfg):
+    """Origins on the bottom side at the exact switch points of the start test
+    (accel.py:219-238: _contains and the flood bound of the edge's other two
+    values), +-1 ulp: the packer's precomputed intervals must agree with the
+    reference rule on both sides of every bound (start, steps, hit bit-exact)."""
+    from oracle import oracle as orc
+    from paper_2112_05570_b200.engine import DeviceMesh
+    paths = fixture_paths(cfg, "mwt")
+    m, om = DeviceMesh.from_files(*paths), orc.Mesh.from_files(*paths)
+    tri = om.tri
+    xy = np.stack([tri.vx, tri.vy], 1)
+    us = []
+    for t in range(len(tri.v)):
+        for i in range(3):
+            P, Q, A = (xy[tri.v[t][(i + 1) % 3]], xy[tri.v[t][(i + 2) % 3]], xy[tri.v[t][i]])
+            if not (P[1] == 0.0 and Q[1] == 0.0 and A[1] > 0.0):
+                continue
+            lo, hi = _dkey(float(min(P[0], Q[0]))) + 1, _dkey(float(max(P[0], Q[0]))) - 1
+            for g in (lambda k: _sa2(Q, A, (_dval(k), 0.0)) > 1e-12,
+                      lambda k: _sa2(A, P, (_dval(k), 0.0)) > 1e-12):
+                if g(lo) == g(hi):
+                    continue
+                k = _switch(g, lo, hi)
+                us += [_dval(k + d) for d in (-2, -1, 0, 1)]
+    assert len(us) >= 16
+    rng = np.random.default_rng(5)
+    th = rng.uniform(0.05, np.pi - 0.05, len(us))
+    rays = np.stack([np.array(us), np.zeros(len(us)), np.cos(th), np.sin(th)], 1)
+    got, ref = m.trace(rays), om.trace(rays)
+    for k in ("start", "seg", "steps"):
+        assert np.array_equal(got[k], ref[k]), k
+    hit = ref["seg"] >= 0
+    assert np.array_equal(got["t"][hit], ref["t"][hit])
+    fast = (got["status"].view(np.uint32) & np.uint32(2048)) != 0
+    assert fast.any() and (~fast).any()  # both sides of the bounds were exercised
