@@ -664,7 +664,14 @@ __device__ __forceinline__ void epilogue(const MeshDev *__restrict__ Mg, const L
 }
 
 
-constexpr int kGrab = 128;  // rays a warp takes from its CTA's counter at a time
+#ifndef MWT_GRAB
+#define MWT_GRAB 128
+#endif
+#ifndef MWT_UNROLL
+#define MWT_UNROLL 5
+#endif
+constexpr int kGrab = MWT_GRAB;  // rays a warp takes from its CTA's counter at a time
+constexpr int kUnroll = MWT_UNROLL;  // fast steps per warp vote
 
 // The trace kernel.  Each CTA owns a contiguous range of rays; its warps take
 // kGrab rays at a time from a shared counter (so all warps of a CTA finish
@@ -854,17 +861,17 @@ __global__ void __launch_bounds__(THREADS, MINB)
         // once the range is exhausted, until none remains.  A lane leaves on a
         // zero apex side (the general rule decides that step), at its stop
         // edge, or at the step guard (walk_step below flags the error).
-        // The guard is checked once per group of 5 steps (a lane enters a
-        // group only with steps < lim - 5, so no step in it passes the guard;
+        // The guard is checked once per group of kUnroll steps (a lane enters a
+        // group only with steps < lim - kUnroll, so no step in it passes the guard;
         // the last few steps before the guard run in walk_step), and the stop
         // edge ends the lane's walk in the loop but its phase is set after it.
-        const int glim = lim - 5;
+        const int glim = lim - kUnroll;
         bool fl = phase == 1 && s.fast && s.steps < glim;
         {
             const int thr = more ? refill_below : 0;
             while (__popc(__ballot_sync(FULL, fl)) > thr) {
 #pragma unroll
-                for (int u2 = 0; u2 < 5; u2++) {
+                for (int u2 = 0; u2 < kUnroll; u2++) {
                     // predicated, not branched: lanes that left compute on record 0
                     // and commit nothing
                     const uint32_t k = fl ? s.w : 0u;
