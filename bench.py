@@ -332,7 +332,10 @@ def main():
         "metric": "rays_per_s_mwt_walk", "value": value, "unit": "rays/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded on-device rays; reference-built Lines-1024 scene + annealed MWT)",
+        "data": f"synthetic (seeded on-device rays; reference-built {args.config} scene + "
+                f"{'annealed MWT' if args.mesh == 'mwt' else 'CDT'})",
+        "parts": [{"rays": ("box_entry" if m == 0 else "interior"), "n": n,
+                   "kernel_ms": kernel_ms[k] / args.steps} for k, (m, n) in enumerate(parts)],
         "config": {"workload": f"{args.config}/{args.mesh}",
                    "rays_per_gpu_per_step": {("box_entry" if m == 0 else "interior"): n for m, n in parts},
                    "triangles": mesh.info.num_triangles, "segments": mesh.info.num_segments,
