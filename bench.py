@@ -335,7 +335,10 @@ def main():
         "data": f"synthetic (seeded on-device rays; reference-built {args.config} scene + "
                 f"{'annealed MWT' if args.mesh == 'mwt' else 'CDT'})",
         "parts": [{"rays": ("box_entry" if m == 0 else "interior"), "n": n,
-                   "kernel_ms": kernel_ms[k] / args.steps} for k, (m, n) in enumerate(parts)],
+                   "stream_ms": kernel_ms[k] / args.steps} for k, (m, n) in enumerate(parts)],
+        "parts_note": "event time on each part's own stream; each persistent launch fills every SM "
+                      "(896 threads x 72 registers), so a later part's time includes waiting for the "
+                      "SMs the earlier one holds",
         "config": {"workload": f"{args.config}/{args.mesh}",
                    "rays_per_gpu_per_step": {("box_entry" if m == 0 else "interior"): n for m, n in parts},
                    "triangles": mesh.info.num_triangles, "segments": mesh.info.num_segments,
