@@ -372,6 +372,20 @@ def main():
         with open(os.path.join(ROOT, "profiles", ns[-1])) as fh:
             line["ncu"] = json.load(fh)
     line["clocks"] = clk.summary()
+    # the roof that binds this kernel (mesh on chip, one ray per thread): warp
+    # instruction issue, 4 per SM per cycle.  Instructions per launch come from
+    # the committed ncu capture of the same launch (same build, same rays).
+    st_ = line.get("ncu") or {}
+    if (args.config, args.mesh) == ("lines1024", "mwt") and st_.get("rays") == n_b and not args.profile:
+        sm_mhz = line["clocks"].get("sm_mhz") or line["clocks"].get("sm_max_mhz") or 1965.0
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        ach = st_["warp_instructions"] / (kms / 1e3) / 1e9
+        pk = sms * 4 * sm_mhz / 1e3
+        line["roofline"]["issue_roof"] = {
+            "achieved": ach, "peak": pk, "unit": "G warp-inst/s", "frac": ach / pk,
+            "warp_inst_per_launch": st_["warp_instructions"], "source": st_.get("report"),
+            "note": "4 warp instructions per SM per cycle at the sampled SM clock; the walk's "
+                    "records come from shared memory, so issue (not HBM) is the binding roof"}
     line["roofline"]["mesh_resident"] = (
         f"shared memory ({mesh.info.walk_smem_bytes} B compact walk table staged per CTA); "
         "HBM carries only per-ray output" if mesh.info.walk_smem_bytes > 0 else

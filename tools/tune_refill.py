@@ -38,8 +38,8 @@ def timeit(reps=15):
     return float(np.median(ts))
 
 
-for minb in (4, 3):
-    for rb in (3, 4, 5, 6, 7, 8, 10):
+for minb in [int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "4,3").split(",")]:
+    for rb in [int(x) for x in (sys.argv[3] if len(sys.argv) > 3 else "3,4,5,6,7,8,10").split(",")]:
         _lib.check(_lib.lib.mwt_set_tuning(rb, minb, 2))
         print(f"{cfg} min_blocks {minb} refill_below {rb:2d}: {timeit():.4f} ms", flush=True)
 _lib.check(_lib.lib.mwt_set_tuning(6, 4, 2))
