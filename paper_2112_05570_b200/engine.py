@@ -24,6 +24,18 @@ def _stream(stream=None):
     return ctypes_void(s.cuda_stream)
 
 
+def _held(t: torch.Tensor | None, stream=None) -> torch.Tensor | None:
+    """``t`` made contiguous; when the kernel runs on a stream other than the
+    current one, a temporary copy is kept alive for that stream's work
+    (record_stream) so the caching allocator does not hand it out early."""
+    if t is None:
+        return None
+    c = t.contiguous()
+    if stream is not None and c.data_ptr() != t.data_ptr():
+        c.record_stream(stream)
+    return c
+
+
 def ctypes_void(v: int):
     import ctypes
     return ctypes.c_void_p(v)
@@ -109,7 +121,7 @@ class DeviceMesh:
         return out
 
     def locate_device(self, pts: torch.Tensor, stream=None):
-        pts = pts.contiguous()
+        pts = _held(pts, stream)
         n = pts.shape[0]
         tid = torch.empty(n, dtype=torch.int32, device=pts.device)
         st = torch.empty(n, dtype=torch.int32, device=pts.device)
@@ -118,7 +130,7 @@ class DeviceMesh:
 
     def trace_device(self, rays: torch.Tensor, start: torch.Tensor | None = None, stream=None,
                      want=("start", "seg", "t", "u", "steps", "status")) -> dict:
-        rays = rays.contiguous()
+        rays, start = _held(rays, stream), _held(start, stream)
         n = rays.shape[0]
         d = rays.device
         out = {}
@@ -127,7 +139,7 @@ class DeviceMesh:
         for k in want:
             out[k] = torch.empty(n, dtype=spec[k], device=d)
         g = out.get
-        check(lib.mwt_trace_dev(self._h, ptr(rays), ptr(start.contiguous()) if start is not None else None,
+        check(lib.mwt_trace_dev(self._h, ptr(rays), ptr(start) if start is not None else None,
                                 n, ptr(g("start")), ptr(g("seg")), ptr(g("t")), ptr(g("u")),
                                 ptr(g("steps")), ptr(g("status")), _stream(stream)), "trace")
         return out
@@ -136,7 +148,7 @@ class DeviceMesh:
                            stream=None) -> dict:
         """Walk and also return each walk's final triangle (``end``), to start
         secondary rays there without a locate (mwt_trace_chain_dev)."""
-        rays = rays.contiguous()
+        rays, start = _held(rays, stream), _held(start, stream)
         n = rays.shape[0]
         d = rays.device
         out = dict(end=torch.empty(n, dtype=torch.int32, device=d),
@@ -146,7 +158,7 @@ class DeviceMesh:
                    steps=torch.empty(n, dtype=torch.int32, device=d),
                    status=torch.empty(n, dtype=torch.int32, device=d))
         check(lib.mwt_trace_chain_dev(self._h, ptr(rays),
-                                      ptr(start.contiguous()) if start is not None else None, n,
+                                      ptr(start) if start is not None else None, n,
                                       ptr(out["end"]), ptr(out["seg"]), ptr(out["t"]), ptr(out["u"]),
                                       ptr(out["steps"]), ptr(out["status"]), _stream(stream)),
               "trace_chain")
@@ -169,7 +181,7 @@ class DeviceMesh:
         return out
 
     def brute_force_device(self, rays: torch.Tensor, stream=None) -> dict:
-        rays = rays.contiguous()
+        rays = _held(rays, stream)
         n = rays.shape[0]
         out = dict(seg=torch.empty(n, dtype=torch.int32, device=rays.device),
                    t=torch.empty(n, dtype=torch.float64, device=rays.device),
@@ -248,7 +260,7 @@ class DeviceBvh:
             pass
 
     def trace_device(self, rays: torch.Tensor, stream=None) -> dict:
-        rays = rays.contiguous()
+        rays = _held(rays, stream)
         n = rays.shape[0]
         d = rays.device
         out = dict(seg=torch.empty(n, dtype=torch.int32, device=d),
@@ -307,7 +319,7 @@ class DeviceKd:
             pass
 
     def trace_device(self, rays: torch.Tensor, stream=None) -> dict:
-        rays = rays.contiguous()
+        rays = _held(rays, stream)
         n = rays.shape[0]
         d = rays.device
         out = dict(seg=torch.empty(n, dtype=torch.int32, device=d),
