@@ -8,6 +8,7 @@ returns.  Outputs (committed): tests/golden/*.npz.
   config_<c>.npz  per BASELINE config: rays, reference start/seg/t/u/steps on cdt & mwt
   struct_<c>.npz  per config: reference bvh/kd results + counters on a ray subset
   hypot.npz     math.hypot values (CPython's is correctly rounded)
+  degenerate.npz  rays where the reference walk and brute force disagree
 
 Usage: python tests/golden/make_golden.py [group ...]
 """
@@ -298,6 +299,47 @@ def make_experiment():
                         csv=np.array(rep.to_csv()), sample5000_seed5=ray_arr(small))
 
 
+# Rays where the reference's walk and its brute-force oracle disagree (so its
+# own run_experiment stops with HitMismatchError): found by tools/paper_table.py
+# over the full BASELINE ray sets on the device; (config, box, raygen index).
+DEGENERATE = [("grass4096", (0.0, 0.0, 1.0, 0.5), 7031414)]
+
+
+def make_degenerate():
+    """The reference walk (both meshes), brute_force_closest and _check on the
+    near-degenerate rays: pins that the engine reproduces the reference's
+    walk result, not the brute-force one, exactly where the two differ."""
+    from mintri.experiment import HitMismatchError, run_experiment
+    out = {}
+    for k, (cfg, box, index) in enumerate(DEGENERATE):
+        d = os.path.join(FIX, cfg)
+        scene = Scene.load(os.path.join(d, "scene.txt"))
+        idx = SceneIndex(scene)
+        arr = raygen(0, box, 0, index, 1)
+        ray = rays_from(arr)[0]
+        bf = brute_force_closest(scene, ray, idx)
+        out[f"{k}_cfg"] = np.array(cfg)
+        out[f"{k}_index"] = np.array(index)
+        out[f"{k}_ray"] = arr
+        out[f"{k}_brute"] = np.array([bf.seg if bf else -1, bf.t if bf else np.nan])
+        tris = []
+        for w in ("cdt", "mwt"):
+            tri = load_triangulation(os.path.join(d, f"{w}.tri"), scene)
+            tris.append(tri)
+            st = TriLocator(tri).locate(ray.origin)
+            hit, stats = traverse_triangulation(tri, ray, st, idx)
+            out[f"{k}_{w}"] = np.array([st, hit.seg if hit else -1, stats.tri_steps])
+            out[f"{k}_{w}_t"] = np.array(hit.t if hit else np.nan)
+        try:
+            run_experiment(scene, tris, [ray], labels=["cdt", "mwt"], ct_grid=[1.0])
+            raised = False
+        except HitMismatchError:
+            raised = True
+        out[f"{k}_harness_raises"] = np.array(raised)
+        print(cfg, index, {kk: v for kk, v in out.items() if kk.startswith(f"{k}_")}, flush=True)
+    np.savez_compressed(os.path.join(HERE, "degenerate.npz"), **out)
+
+
 if __name__ == "__main__":
     groups = sys.argv[1:] or ["known", "hypot"] + [f"config:{c}" for c in CONFIGS] + \
         [f"struct:{c}" for c in CONFIGS[1:]]
@@ -308,6 +350,8 @@ if __name__ == "__main__":
             make_hypot()
         elif g == "experiment":
             make_experiment()
+        elif g == "degenerate":
+            make_degenerate()
         elif g.startswith("config:"):
             make_config(g.split(":", 1)[1])
         elif g.startswith("struct:"):

@@ -103,3 +103,33 @@ def test_structures_on_device(cfg):
         assert np.array_equal(o["nodes"][ok], g[f"kd{tag}_nodes"][ok])
         assert np.array_equal(o["ropes"][ok], g[f"kd{tag}_ropes"][ok])
         assert np.array_equal(o["prims"][ok], g[f"kd{tag}_prims"][ok])
+
+
+def test_degenerate_rays_on_device():
+    """The rays where the reference walk and brute force disagree
+    (tests/golden/degenerate.npz): the device walk returns the reference walk's
+    answer -- through the host API, from the explicit rays, and fused with the
+    on-device ray generator at the ray's own index -- and the device brute
+    force the reference brute force's."""
+    import torch
+    from paper_2112_05570_b200.engine import DeviceMesh, new_histogram
+    g = _golden("degenerate.npz")
+    k = 0
+    while f"{k}_cfg" in g:
+        cfg, index = str(g[f"{k}_cfg"]), int(g[f"{k}_index"])
+        box = (0.0, 0.0, 1.0, 0.5) if cfg == "grass4096" else (0.0, 0.0, 1.0, 1.0)
+        ray = g[f"{k}_ray"]
+        for w in ("cdt", "mwt"):
+            m = DeviceMesh.from_files(*fixture_paths(cfg, w))
+            assert np.array_equal(m.raygen(0, box, 0, index, 1).view(np.uint64), ray.view(np.uint64))
+            o = m.trace(ray)
+            start, seg, steps = (int(x) for x in g[f"{k}_{w}"])
+            assert (int(o["start"][0]), int(o["seg"][0]), int(o["steps"][0])) == (start, seg, steps)
+            assert o["t"][0] == float(g[f"{k}_{w}_t"])
+            gen = m.trace_generated_device(0, box, 0, index, 1, True, new_histogram())
+            torch.cuda.synchronize()
+            assert (int(gen["seg"][0]), int(gen["steps"][0])) == (seg, steps)
+            bf = m.brute_force(ray)
+            assert int(bf["seg"][0]) == int(g[f"{k}_brute"][0]) and bf["t"][0] == g[f"{k}_brute"][1]
+        k += 1
+    assert k > 0

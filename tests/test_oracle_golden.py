@@ -183,3 +183,29 @@ def test_raygen_box_entry_is_a_uniform_line_field(box):
         proj = nx[:, None] * cx[None, :] + ny[:, None] * cy[None, :]
         a, b = proj.min(1), proj.max(1)
         assert kstest((s - a) / (b - a), "uniform").pvalue > 1e-4, lo
+
+
+def test_degenerate_rays_reference_walk_not_brute_force():
+    """Rays where the reference's walk and its brute-force oracle disagree (its
+    run_experiment raises HitMismatchError on them; found over the full
+    BASELINE ray sets): the oracle reproduces the reference walk's start, hit,
+    t and steps, and the reference brute force, each bit for bit."""
+    g = _golden("degenerate.npz")
+    k = 0
+    while f"{k}_cfg" in g:
+        cfg, index = str(g[f"{k}_cfg"]), int(g[f"{k}_index"])
+        box = (0.0, 0.0, 1.0, 0.5) if cfg == "grass4096" else (0.0, 0.0, 1.0, 1.0)
+        ray = rg.raygen(0, box, 0, index, 1)
+        assert np.array_equal(ray.view(np.uint64), g[f"{k}_ray"].view(np.uint64))
+        assert bool(g[f"{k}_harness_raises"])
+        for w in ("cdt", "mwt"):
+            om = orc.Mesh.from_files(*fixture_paths(cfg, w))
+            o = om.trace(ray)
+            start, seg, steps = (int(x) for x in g[f"{k}_{w}"])
+            assert (int(o["start"][0]), int(o["seg"][0]), int(o["steps"][0])) == (start, seg, steps)
+            assert o["t"][0] == float(g[f"{k}_{w}_t"])
+        bf = om.brute_force(ray)
+        assert int(bf["seg"][0]) == int(g[f"{k}_brute"][0]) != seg
+        assert bf["t"][0] == g[f"{k}_brute"][1]
+        k += 1
+    assert k > 0
