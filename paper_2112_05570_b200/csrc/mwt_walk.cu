@@ -607,27 +607,34 @@ __device__ __forceinline__ Init prologue_body(const MeshDev &M, const BTab &T, c
 
 // Block-private histogram: a shared atomic per lane for its step bin,
 // warp-aggregated updates for hit / miss / the step sum / each status bit present.
+template <int NT>  // threads per CTA
 struct HistSm {
     unsigned int bins[MWT_HIST_LEN];
     unsigned long long steps_sum;
     unsigned long long warp_steps[32];  // per-warp partial step sums (owner-only updates)
     unsigned warp_hm[32][2];            // per-warp hit / miss counts (owner-only updates)
+    // per-thread counters (owner-only, no collectives): hits | misses << 21 |
+    // boundary starts << 42, and the step sum
+    unsigned long long lane_cnt[NT];
+    unsigned long long lane_steps[NT];
 };
+constexpr unsigned long long kLaneHit = 1ull, kLaneMiss = 1ull << 21, kLaneBnd = 1ull << 42;
 
-__device__ __forceinline__ void hist_add_warp(HistSm *H, int seg, int steps, uint32_t st) {
-    const unsigned m = __activemask();
-    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+template <int NT>
+__device__ __forceinline__ void hist_add_warp(HistSm<NT> *H, int seg, int steps, uint32_t st) {
     const int bin = steps < MWT_HIST_STEP_BINS - 1 ? (steps < 0 ? 0 : steps) : MWT_HIST_STEP_BINS - 1;
     atomicAdd(H->bins + bin, 1u);  // per lane: cheaper than grouping equal bins (match.any)
-    const unsigned hits = __ballot_sync(m, seg >= 0);
-    const unsigned ssum = __reduce_add_sync(m, (unsigned)(steps > 0 ? steps : 0));
-    unsigned any = __reduce_or_sync(m, st) & 0xFFFu;
-    if (lane == leader) {
-        const int w = threadIdx.x >> 5;  // this warp's own slots: no atomics
-        H->warp_hm[w][0] += (unsigned)__popc(hits);
-        H->warp_hm[w][1] += (unsigned)__popc(m & ~hits);
-        H->warp_steps[w] += (unsigned long long)ssum;
-    }
+    // hit / miss / boundary-start counts and the step sum: this thread's own
+    // slots (flushed once per CTA)
+    H->lane_cnt[threadIdx.x] += (seg >= 0 ? kLaneHit : kLaneMiss) +
+                                ((st & MWT_ST_BOUNDARY) ? kLaneBnd : 0ull);
+    H->lane_steps[threadIdx.x] += (unsigned long long)(steps > 0 ? steps : 0);
+    // the other status bits are rare: warp-aggregated when present
+    const unsigned rest = st & 0x7FFu;
+    const unsigned m = __activemask();
+    if (!__any_sync(m, rest)) return;
+    const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+    unsigned any = __reduce_or_sync(m, rest);
     while (any) {
         const int b = __ffs(any) - 1;
         any &= any - 1;
@@ -638,9 +645,9 @@ __device__ __forceinline__ void hist_add_warp(HistSm *H, int seg, int steps, uin
 
 // Epilogue for a lane whose ray has ended (phase 2: exit edge
 // reached; phase 3: TraversalError): hit test, per-ray outputs, histogram.
-template <bool END>
+template <bool END, int NT>
 __device__ __forceinline__ void epilogue(const MeshDev *__restrict__ Mg, const Launch *__restrict__ L,
-                                      HistSm *H, const double4 *sseg, long long i, double ox, double oy, double dx,
+                                      HistSm<NT> *H, const double4 *sseg, long long i, double ox, double oy, double dx,
                                       double dy, int kr, int ch, uint32_t w,
                                       uint32_t st, int steps, int phase) {
     int seg = -1;
@@ -729,7 +736,7 @@ template <bool GEN, int MINB, int THREADS, bool SMEM, bool STAGE = SMEM, bool TR
 __global__ void __launch_bounds__(THREADS, MINB)
     k_trace(const __grid_constant__ MeshDev M, const __grid_constant__ Launch L, long long n,
             long long *hist, int refill_below) {
-    __shared__ HistSm H;
+    __shared__ HistSm<THREADS> H;
     __shared__ unsigned s_next;
     extern __shared__ __align__(16) unsigned char dsm[];
     const uint2 *srec = reinterpret_cast<const uint2 *>(dsm);
@@ -775,8 +782,11 @@ __global__ void __launch_bounds__(THREADS, MINB)
     const long long per = (n + gridDim.x - 1) / gridDim.x;
     const long long cbeg = (long long)blockIdx.x * per;
     const long long cend = cbeg + per < n ? cbeg + per : n;
-    if (hist)
+    if (hist) {
         for (int k = threadIdx.x; k < MWT_HIST_LEN; k += THREADS) H.bins[k] = 0u;
+        H.lane_cnt[threadIdx.x] = 0ull;
+        H.lane_steps[threadIdx.x] = 0ull;
+    }
     if (threadIdx.x == 0) {
         H.steps_sum = 0ull;
         for (int w = 0; w < 32; w++) {
@@ -786,7 +796,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         s_next = 0u;
     }
     __syncthreads();
-    HistSm *Hp = hist ? &H : nullptr;
+    HistSm<THREADS> *Hp = hist ? &H : nullptr;
     const unsigned FULL = 0xffffffffu;
     const int lane = threadIdx.x & 31;
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -809,7 +819,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
         unsigned walking = __ballot_sync(FULL, phase == 1);
         if (__popc(walking) <= refill_below) {
             if (phase >= 2) {
-                epilogue<!GEN>(&M, &L, Hp, sseg, cbeg + (long long)idx, r.ox, r.oy, r.dx, r.dy, s.kr, s.ch, s.w, st,
+                epilogue<!GEN, THREADS>(&M, &L, Hp, sseg, cbeg + (long long)idx, r.ox, r.oy, r.dx, r.dy, s.kr, s.ch, s.w, st,
                          s.steps, phase);
                 phase = 0;
             }
@@ -924,6 +934,25 @@ __global__ void __launch_bounds__(THREADS, MINB)
         }
     }
     if (hist) {
+        {  // this thread's counters into its warp's slots, then the CTA flush
+            const unsigned long long c = H.lane_cnt[threadIdx.x];
+            unsigned hh = (unsigned)(c & 0x1FFFFFu), mm = (unsigned)((c >> 21) & 0x1FFFFFu),
+                     bb = (unsigned)(c >> 42);
+            unsigned long long ss = H.lane_steps[threadIdx.x];
+            for (int o = 16; o > 0; o >>= 1) {
+                hh += __shfl_down_sync(FULL, hh, o);
+                mm += __shfl_down_sync(FULL, mm, o);
+                bb += __shfl_down_sync(FULL, bb, o);
+                ss += __shfl_down_sync(FULL, ss, o);
+            }
+            if (lane == 0) {
+                const int w = threadIdx.x >> 5;
+                H.warp_hm[w][0] += hh;
+                H.warp_hm[w][1] += mm;
+                H.warp_steps[w] += ss;
+                if (bb) atomicAdd(H.bins + MWT_HIST_STATUS0 + 11, bb);
+            }
+        }
         __syncthreads();
         for (int k = threadIdx.x; k < MWT_HIST_LEN; k += THREADS)
             if (H.bins[k] && k != MWT_HIST_STEPS_SUM)
