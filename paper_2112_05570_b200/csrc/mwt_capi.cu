@@ -334,10 +334,8 @@ int mwt_trace_host(const mwt_mesh *cm, const double *rays, const int32_t *start,
     // engines) and the kernels.  With pinned host buffers the call is bounded by
     // the larger copy direction.
     const int64_t chunk = n < kHostChunk ? n : kHostChunk;
-    const size_t per = 32 + 4 + 4 + 4 + 8 + 8 + 4 + 4;  // rays, start, 6 outputs
     const size_t slot = Arena::align((size_t)chunk * 32) + 7 * Arena::align((size_t)chunk * 8);
     const size_t need = kHostStreams * slot;
-    (void)per;
     if (need > m->scratch_bytes) {
         if (m->scratch) cudaFree(m->scratch);
         m->scratch = nullptr;
@@ -347,6 +345,18 @@ int mwt_trace_host(const mwt_mesh *cm, const double *rays, const int32_t *start,
     }
     for (int k = 0; k < kHostStreams; k++)
         if (!m->hstream[k]) CK(cudaStreamCreateWithFlags(&m->hstream[k], cudaStreamNonBlocking));
+    // on an error, wait for the chunks already queued: they read and write the
+    // caller's host buffers, which must not be in use after we return
+    auto drain = [&](cudaError_t e, const char *what) {
+        for (int k = 0; k < kHostStreams; k++)
+            if (m->hstream[k]) (void)cudaStreamSynchronize(m->hstream[k]);
+        return cuda_fail(e, what);
+    };
+#define MWT_CKQ(expr)                                  \
+    do {                                               \
+        cudaError_t _e = (expr);                       \
+        if (_e != cudaSuccess) return drain(_e, #expr); \
+    } while (0)
     const int64_t nchunks = (n + chunk - 1) / chunk;
     for (int64_t c = 0; c < nchunks; c++) {
         const int k = (int)(c % kHostStreams);
@@ -363,20 +373,21 @@ int mwt_trace_host(const mwt_mesh *cm, const double *rays, const int32_t *start,
         int32_t *d_steps = carve<int32_t>(a, chunk);
         uint32_t *d_st = carve<uint32_t>(a, chunk);
         cudaStream_t s = m->hstream[k];
-        CK(cudaMemcpyAsync(d_rays, rays + 4 * off, 32 * (size_t)cnt, cudaMemcpyHostToDevice, s));
-        if (start) CK(cudaMemcpyAsync(d_start, start + off, 4 * (size_t)cnt, cudaMemcpyHostToDevice, s));
+        MWT_CKQ(cudaMemcpyAsync(d_rays, rays + 4 * off, 32 * (size_t)cnt, cudaMemcpyHostToDevice, s));
+        if (start) MWT_CKQ(cudaMemcpyAsync(d_start, start + off, 4 * (size_t)cnt, cudaMemcpyHostToDevice, s));
         int rc = mwt::launch_trace(m->dev, d_rays, start ? d_start : nullptr, cnt,
                                    out_start ? d_ostart : nullptr, out_seg ? d_seg : nullptr,
                                    out_t ? d_t : nullptr, out_u ? d_u : nullptr,
                                    out_steps ? d_steps : nullptr, out_status ? d_st : nullptr, s);
-        if (rc) return cuda_fail((cudaError_t)rc, "trace_host launch");
-        if (out_start) CK(cudaMemcpyAsync(out_start + off, d_ostart, 4 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
-        if (out_seg) CK(cudaMemcpyAsync(out_seg + off, d_seg, 4 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
-        if (out_t) CK(cudaMemcpyAsync(out_t + off, d_t, 8 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
-        if (out_u) CK(cudaMemcpyAsync(out_u + off, d_u, 8 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
-        if (out_steps) CK(cudaMemcpyAsync(out_steps + off, d_steps, 4 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
-        if (out_status) CK(cudaMemcpyAsync(out_status + off, d_st, 4 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
+        if (rc) return drain((cudaError_t)rc, "trace_host launch");
+        if (out_start) MWT_CKQ(cudaMemcpyAsync(out_start + off, d_ostart, 4 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
+        if (out_seg) MWT_CKQ(cudaMemcpyAsync(out_seg + off, d_seg, 4 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
+        if (out_t) MWT_CKQ(cudaMemcpyAsync(out_t + off, d_t, 8 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
+        if (out_u) MWT_CKQ(cudaMemcpyAsync(out_u + off, d_u, 8 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
+        if (out_steps) MWT_CKQ(cudaMemcpyAsync(out_steps + off, d_steps, 4 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
+        if (out_status) MWT_CKQ(cudaMemcpyAsync(out_status + off, d_st, 4 * (size_t)cnt, cudaMemcpyDeviceToHost, s));
     }
+#undef MWT_CKQ
     for (int k = 0; k < kHostStreams; k++) CK(cudaStreamSynchronize(m->hstream[k]));
     return MWT_OK;
 }
