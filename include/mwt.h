@@ -205,6 +205,20 @@ int mwt_kd_trace_dev(const mwt_kd *kd, const double *rays, int64_t n, int32_t *o
 int mwt_brute_force_dev(const mwt_mesh *mesh, const double *rays, int64_t n, int32_t *out_seg,
                         double *out_t, double *out_u, void *stream);
 
+/* One process, several GPUs (SURVEY.md §8b `mwt_run_sharded`; the reference is
+ * single-process, accel.py has no counterpart).  `meshes[k]` is the same mesh
+ * created on device k (ndev <= 64); rays [first, first + n) -- or the host
+ * rays -- split into contiguous near-equal ranges, one per device, each driven
+ * by its own host thread and stream; results are those of one device.
+ * mwt_trace_generated_sharded sums the per-device histograms into hist_out
+ * (host int64[MWT_HIST_LEN]); mwt_trace_host_sharded writes the per-ray host
+ * outputs like mwt_trace_host.  Synchronous. */
+int mwt_trace_generated_sharded(const mwt_mesh *const *meshes, int ndev, int mode, const double *box,
+                                uint64_t seed, uint64_t first, int64_t n, int64_t *hist_out);
+int mwt_trace_host_sharded(const mwt_mesh *const *meshes, int ndev, const double *rays,
+                           const int32_t *start, int64_t n, int32_t *out_start, int32_t *out_seg,
+                           double *out_t, double *out_u, int32_t *out_steps, uint32_t *out_status);
+
 #ifdef __cplusplus
 }
 #endif

@@ -83,6 +83,8 @@ SIGNATURES = {
     "mwt_kd_destroy": (INT, [P]),
     "mwt_kd_trace_dev": (INT, [P, P, I64, P, P, P, P, P, P, P, P]),
     "mwt_brute_force_dev": (INT, [P, P, I64, P, P, P, P]),
+    "mwt_trace_generated_sharded": (INT, [P, INT, INT, P, U64, U64, I64, P]),
+    "mwt_trace_host_sharded": (INT, [P, INT, P, P, I64, P, P, P, P, P, P]),
 }
 
 

@@ -5,6 +5,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "mwt_internal.h"
@@ -579,6 +580,96 @@ int mwt_brute_force_dev(const mwt_mesh *m, const double *rays, int64_t n, int32_
     DeviceGuard g(m->device);
     int rc = mwt::launch_brute(m->dev, rays, n, out_seg, out_t, out_u, stream);
     if (rc) return cuda_fail((cudaError_t)rc, "brute_force launch");
+    return MWT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// One process, several GPUs (SURVEY.md §8b `mwt_run_sharded`): rays shard by
+// global index into contiguous ranges, one host thread per device drives its
+// own stream, and the per-device histograms are summed on the host -- the
+// single-process counterpart of the bench's one-process-per-GPU NCCL path.
+
+namespace {
+struct ShardErr {
+    int rc = MWT_OK;
+    std::string msg;
+};
+
+// contiguous near-equal ranges [floor(k*n/d), floor((k+1)*n/d))
+inline int64_t shard_lo(int64_t n, int ndev, int k) { return (int64_t)((__int128)n * k / ndev); }
+
+int shard_args_ok(const mwt_mesh *const *meshes, int ndev) {
+    if (!meshes || ndev <= 0 || ndev > 64) return 0;
+    for (int k = 0; k < ndev; k++)
+        if (!meshes[k] || meshes[k]->dev.nt == 0) return 0;
+    return 1;
+}
+}  // namespace
+
+int mwt_trace_generated_sharded(const mwt_mesh *const *meshes, int ndev, int mode, const double *box,
+                                uint64_t seed, uint64_t first, int64_t n, int64_t *hist_out) {
+    if (!shard_args_ok(meshes, ndev) || !box || n < 0 || !hist_out ||
+        (mode != MWT_RAYS_BOX_ENTRY && mode != MWT_RAYS_INTERIOR))
+        return fail(MWT_E_INVALID, "trace_generated_sharded: bad argument");
+    std::vector<std::vector<int64_t>> part(ndev, std::vector<int64_t>(MWT_HIST_LEN, 0));
+    std::vector<ShardErr> err(ndev);
+    std::vector<std::thread> th;
+    for (int k = 0; k < ndev; k++)
+        th.emplace_back([&, k]() {
+            mwt_mesh *m = const_cast<mwt_mesh *>(meshes[k]);
+            const int64_t lo = shard_lo(n, ndev, k), cnt = shard_lo(n, ndev, k + 1) - lo;
+            std::lock_guard<std::mutex> lk(m->mu);
+            DeviceGuard g(m->device);
+            long long *dh = nullptr;
+            cudaError_t e = g.ok ? cudaSuccess : cudaErrorInvalidDevice;
+            if (e == cudaSuccess) e = cudaMalloc(&dh, sizeof(long long) * MWT_HIST_LEN);
+            if (e == cudaSuccess) e = cudaMemsetAsync(dh, 0, sizeof(long long) * MWT_HIST_LEN, m->stream);
+            if (e == cudaSuccess && cnt > 0)
+                e = (cudaError_t)mwt::launch_trace_generated(m->dev, mode, box, seed, first + (uint64_t)lo,
+                                                             cnt, nullptr, nullptr, nullptr, dh, m->stream);
+            if (e == cudaSuccess)
+                e = cudaMemcpyAsync(part[k].data(), dh, sizeof(long long) * MWT_HIST_LEN,
+                                    cudaMemcpyDeviceToHost, m->stream);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(m->stream);
+            if (dh) cudaFree(dh);
+            if (e != cudaSuccess) {
+                err[k].rc = MWT_E_CUDA;
+                err[k].msg = std::string("device ") + std::to_string(m->device) + ": " + cudaGetErrorName(e);
+            }
+        });
+    for (auto &t : th) t.join();
+    for (int k = 0; k < ndev; k++)
+        if (err[k].rc) return fail(err[k].rc, "trace_generated_sharded: " + err[k].msg);
+    for (int b = 0; b < MWT_HIST_LEN; b++) {
+        int64_t sum = 0;
+        for (int k = 0; k < ndev; k++) sum += part[k][b];
+        hist_out[b] = sum;
+    }
+    return MWT_OK;
+}
+
+int mwt_trace_host_sharded(const mwt_mesh *const *meshes, int ndev, const double *rays,
+                           const int32_t *start, int64_t n, int32_t *out_start, int32_t *out_seg,
+                           double *out_t, double *out_u, int32_t *out_steps, uint32_t *out_status) {
+    if (!shard_args_ok(meshes, ndev) || n < 0 || (n > 0 && !rays))
+        return fail(MWT_E_INVALID, "trace_host_sharded: bad argument");
+    std::vector<ShardErr> err(ndev);
+    std::vector<std::thread> th;
+    for (int k = 0; k < ndev; k++)
+        th.emplace_back([&, k]() {
+            const int64_t lo = shard_lo(n, ndev, k), cnt = shard_lo(n, ndev, k + 1) - lo;
+            auto at = [lo](auto *p, int w) { return p ? p + lo * w : p; };
+            const int rc = mwt_trace_host(meshes[k], rays + 4 * lo, at(start, 1), cnt, at(out_start, 1),
+                                          at(out_seg, 1), at(out_t, 1), at(out_u, 1), at(out_steps, 1),
+                                          at(out_status, 1));
+            if (rc) {
+                err[k].rc = rc;
+                err[k].msg = g_err;  // this worker thread's message
+            }
+        });
+    for (auto &t : th) t.join();
+    for (int k = 0; k < ndev; k++)
+        if (err[k].rc) return fail(err[k].rc, "trace_host_sharded: " + err[k].msg);
     return MWT_OK;
 }
 

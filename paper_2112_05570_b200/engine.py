@@ -341,6 +341,40 @@ class DeviceKd:
         return {k: v.cpu().numpy() for k, v in out.items()}
 
 
+def _handles(meshes):
+    import ctypes
+    arr = (ctypes.c_void_p * len(meshes))(*[m.handle.value for m in meshes])
+    return arr
+
+
+def trace_generated_sharded(meshes, mode: int, box, seed: int, first: int, n: int) -> np.ndarray:
+    """Rays [first, first+n) split over ``meshes`` (the same mesh on each
+    device), one host thread per device; returns the summed histogram
+    (mwt_trace_generated_sharded)."""
+    import ctypes
+    h = np.zeros(_lib.HIST_LEN, np.int64)
+    arr = _handles(meshes)
+    check(lib.mwt_trace_generated_sharded(ctypes.cast(arr, ctypes.c_void_p), len(meshes), int(mode),
+                                          ptr(_f64(box)), int(seed), int(first), int(n), ptr(h)),
+          "trace_generated_sharded")
+    return h
+
+
+def trace_sharded(meshes, rays: np.ndarray, start: np.ndarray | None = None) -> dict:
+    """Host rays split over ``meshes`` (mwt_trace_host_sharded)."""
+    import ctypes
+    rays = _f64(rays).reshape(-1, 4)
+    n = len(rays)
+    out = dict(start=np.empty(n, np.int32), seg=np.empty(n, np.int32), t=np.empty(n),
+               u=np.empty(n), steps=np.empty(n, np.int32), status=np.empty(n, np.uint32))
+    s = _i32(start) if start is not None else None
+    arr = _handles(meshes)
+    check(lib.mwt_trace_host_sharded(ctypes.cast(arr, ctypes.c_void_p), len(meshes), ptr(rays), ptr(s), n,
+                                     ptr(out["start"]), ptr(out["seg"]), ptr(out["t"]), ptr(out["u"]),
+                                     ptr(out["steps"]), ptr(out["status"])), "trace_host_sharded")
+    return out
+
+
 def new_histogram(device: int = 0) -> torch.Tensor:
     return torch.zeros(_lib.HIST_LEN, dtype=torch.int64, device=torch.device("cuda", device))
 

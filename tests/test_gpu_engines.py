@@ -343,3 +343,31 @@ def test_box_entry_start_at_interval_bounds(cfg):
     assert np.array_equal(got["t"][hit], ref["t"][hit])
     fast = (got["status"].view(np.uint32) & np.uint32(2048)) != 0
     assert fast.any() and (~fast).any()  # both sides of the bounds were exercised
+
+
+@pytest.mark.parametrize("ndev", [1, 2, 3])
+def test_single_process_sharded_entry_points(ndev):
+    """mwt_trace_generated_sharded / mwt_trace_host_sharded (one host thread
+    and stream per device handle; here ndev handles of the same mesh, all on
+    cuda:0 of this one-GPU box): the summed histogram and the per-ray outputs
+    equal one unsharded call."""
+    import torch
+    from paper_2112_05570_b200.engine import (DeviceMesh, new_histogram, trace_generated_sharded,
+                                              trace_sharded)
+    from paper_2112_05570_b200.sharding import histogram_host
+    paths = fixture_paths("lines1024", "mwt")
+    meshes = [DeviceMesh.from_files(*paths) for _ in range(ndev)]
+    n = 300001
+    h1 = new_histogram()
+    meshes[0].trace_generated_device(0, (0, 0, 1, 1), 9, 123, n, False, h1)
+    torch.cuda.synchronize()
+    hs = trace_generated_sharded(meshes, 0, (0, 0, 1, 1), 9, 123, n)
+    assert np.array_equal(hs, h1.cpu().numpy())
+    rays = meshes[0].raygen(1, (0, 0, 1, 1), 9, 5, 100003)
+    a, b = meshes[0].trace(rays), trace_sharded(meshes, rays)
+    for k in ("start", "seg", "steps", "status"):
+        assert np.array_equal(a[k], b[k]), k
+    hit = a["seg"] >= 0
+    assert np.array_equal(a["t"][hit], b["t"][hit]) and np.array_equal(a["u"][hit], b["u"][hit])
+    assert np.array_equal(histogram_host(b["seg"], b["steps"], b["status"])[:1027],
+                          histogram_host(a["seg"], a["steps"], a["status"])[:1027])
