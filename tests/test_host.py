@@ -35,6 +35,19 @@ def test_invalid_arguments_fail_loudly():
     with pytest.raises(_lib.MwtError):
         _lib.check(rc, "mesh_create")
     assert _lib.lib.mwt_trace_host(None, None, None, 1, None, None, None, None, None, None) == -1
+    # the single-process sharded entry points validate before touching a device
+    h = np.zeros(_lib.HIST_LEN, np.int64)
+    box = np.array([0.0, 0.0, 1.0, 1.0])
+    assert _lib.lib.mwt_trace_generated_sharded(None, 1, 0, _lib.ptr(box), 0, 0, 10, _lib.ptr(h)) == -1
+    assert b"trace_generated_sharded" in _lib.lib.mwt_last_error()
+    none2 = (ctypes.c_void_p * 2)(None, None)
+    assert _lib.lib.mwt_trace_generated_sharded(ctypes.cast(none2, ctypes.c_void_p), 2, 0, _lib.ptr(box),
+                                                0, 0, 10, _lib.ptr(h)) == -1
+    assert _lib.lib.mwt_trace_generated_sharded(ctypes.cast(none2, ctypes.c_void_p), 0, 0, _lib.ptr(box),
+                                                0, 0, 10, _lib.ptr(h)) == -1
+    assert _lib.lib.mwt_trace_host_sharded(None, 1, None, None, 5, None, None, None, None, None,
+                                           None) == -1
+    assert b"trace_host_sharded" in _lib.lib.mwt_last_error()
 
 
 def test_product_never_imports_the_oracle():
