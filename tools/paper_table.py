@@ -34,6 +34,8 @@ CONFIGS = {  # BASELINE.json configs: ray box and box-entry ray count
     "grass4096": ((0.0, 0.0, 1.0, 0.5), 1 << 24),
     "hair512": ((0.0, 0.0, 1.0, 1.0), 1 << 24),
     "floorplan64": ((0.0, 0.0, 1.0, 1.0), 1 << 26),
+    # Lines-1024's 2^22 "recursive" rays: origins uniform in the box (point-location path)
+    "lines1024-interior": ((0.0, 0.0, 1.0, 1.0), 1 << 22),
 }
 SEED = 0
 
@@ -62,11 +64,12 @@ experiment.check_hits = _recording_check
 
 def run(cfg: str) -> dict:
     box, n = CONFIGS[cfg]
-    d = os.path.join(ROOT, "fixtures", "data", cfg)
+    mode = 1 if cfg.endswith("-interior") else 0
+    d = os.path.join(ROOT, "fixtures", "data", cfg.split("-")[0])
     scene = Scene.load(os.path.join(d, "scene.txt"))
     tris = [load_triangulation(os.path.join(d, f"{w}.tri"), scene) for w in ("cdt", "mwt")]
     rays = DeviceMesh.from_files(os.path.join(d, "scene.txt"), os.path.join(d, "mwt.tri")).raygen(
-        0, box, SEED, 0, n)
+        mode, box, SEED, 0, n)
     t0 = time.perf_counter()
     if os.path.exists(os.path.join(d, "bvh_ct1.npz")):
         bvh = {c: load_structure(os.path.join(d, f"bvh_ct{c:g}.npz")) for c in GRID}
