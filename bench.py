@@ -386,6 +386,17 @@ def main():
             "warp_inst_per_launch": st_["warp_instructions"], "source": st_.get("report"),
             "note": "4 warp instructions per SM per cycle at the sampled SM clock; the walk's "
                     "records come from shared memory, so issue (not HBM) is the binding roof"}
+    if mesh.info.walk_smem_bytes == 0 and not args.profile:
+        # walk records from global memory: one L1 data-pipe wavefront per lane
+        # per step (scattered 32-B records), one wavefront per SM per cycle
+        sm_mhz = line["clocks"].get("sm_mhz") or line["clocks"].get("sm_max_mhz") or 1965.0
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        ach = hb["steps_sum"] / (kms / 1e3) / 1e9
+        pk = sms * sm_mhz / 1e3
+        line["roofline"]["l1_wavefront_roof"] = {
+            "achieved": ach, "peak": pk, "unit": "G lane-steps/s", "frac": ach / pk,
+            "note": "walk records read from L1/L2 (the mesh does not fit shared memory): each step is "
+                    "one scattered 32-B load = one L1 wavefront; the pipe retires one per SM per cycle"}
     line["roofline"]["mesh_resident"] = (
         f"shared memory ({mesh.info.walk_smem_bytes} B compact walk table staged per CTA); "
         "HBM carries only per-ray output" if mesh.info.walk_smem_bytes > 0 else
