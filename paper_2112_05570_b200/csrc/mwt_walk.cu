@@ -1102,6 +1102,9 @@ static void launch_k_trace_any(const MeshDev &m, const Launch &L, long long n, l
     if (g_variant >= 2 && launch_k_trace<GEN, 1, 896, true, true, true>(m, L, n, hist, stream)) return;
     // global walk records; boundary table (and segments when they fit) staged
     if (g_variant >= 2 && launch_k_trace<GEN, 1, 896, false, true>(m, L, n, hist, stream)) return;
+    // nothing fits shared memory (Grass-4096's 4,108-edge boundary table): the
+    // same 896-thread persistent CTAs reading every table from L1/L2
+    if (g_variant >= 2 && launch_k_trace<GEN, 1, 896, false, false>(m, L, n, hist, stream)) return;
     if (g_min_blocks == 3)
         launch_k_trace<GEN, 3, kThreads, false>(m, L, n, hist, stream);
     else if (g_min_blocks == 2)
