@@ -59,6 +59,19 @@ extern "C" {
 /* ray generator modes (engine-defined) */
 #define MWT_RAYS_BOX_ENTRY 0   /* isotropic lines through the box, origin at box entry */
 #define MWT_RAYS_INTERIOR 1    /* origin uniform in the box, isotropic direction */
+/* Coherent ray order: a mode word base | group_log2 << 8 | cell_bits << 16.
+ * Every 64-bit draw of ray i keeps its own low bits and takes the top
+ * `cell_bits` of each 32-bit half from the same draw of its group's stream
+ * (group = i >> group_log2).  Each ray is still an exact draw of the base
+ * distribution (its draws remain uniform words); rays of one group share a
+ * cell of the direction draw and of the entry-point draw, so a warp's rays run
+ * nearly the same line.  cell_bits = 0 is the iid
+ * generator; cell_bits <= 16, group_log2 <= 40. */
+#define MWT_RAYS_COHERENT(base, group_log2, cell_bits) \
+    ((base) | ((group_log2) << 8) | ((cell_bits) << 16))
+/* the benchmark's ordering: groups of 512 rays (four warp grabs), 12 shared bits per coordinate */
+#define MWT_RAYS_BOX_ENTRY_COHERENT MWT_RAYS_COHERENT(MWT_RAYS_BOX_ENTRY, 9, 12)
+#define MWT_RAYS_INTERIOR_COHERENT MWT_RAYS_COHERENT(MWT_RAYS_INTERIOR, 9, 12)
 
 /* histogram layout written by mwt_trace_generated_dev / mwt_histogram_dev */
 #define MWT_HIST_STEP_BINS 1024 /* bins 0..1022 exact step counts, 1023 = overflow */
@@ -98,6 +111,12 @@ int mwt_device_count(int *count);
  * the per-triangle table first (A/B); variant 1 always
  * walks from global memory with 256-thread CTAs, `min_blocks_per_sm` CTAs per SM. */
 int mwt_set_tuning(int refill_below, int min_blocks_per_sm, int variant);
+
+/* Measurement helper (no reference counterpart): L2 read bandwidth of
+ * `device`, streaming 128-bit ld.global.cg loads over an L2-resident buffer of
+ * `bytes` (1 MiB .. 1 GiB) `passes` times from every SM -- the on-chip roof the
+ * walk's algorithmic bytes are compared with.  Synchronous. */
+int mwt_probe_l2_read(int device, int64_t bytes, int passes, double *gbs_out);
 
 /* K1 -- mesh packer.
  * Replaces: building `Triangulation` + `SceneIndex` for the walk

@@ -144,14 +144,45 @@ static inline uint64_t mix64(uint64_t z) {
 uint64_t orc_ray_key(uint64_t seed, uint64_t stream) {
     return mix64(mix64(seed + GOLDEN) ^ (stream * 0xD1B54A32D192ED03ull));
 }
-/* mode 0: box-entry isotropic line rays; mode 1: interior origins */
-void orc_raygen_one(int mode, const double box[4], uint64_t key, uint64_t idx, double out[4]) {
-    uint64_t s0 = key ^ idx; /* per-ray SplitMix64 stream: mix64(s0 + (k + 1) * golden) */
+/* A mode word (include/mwt.h): base | group_log2 << 8 | cell_bits << 16.
+ * Base 0: box-entry isotropic line rays; 1: interior origins.  With
+ * cell_bits c > 0 ("coherent" order) every draw k of ray i takes the top c
+ * bits of each 32-bit half from draw k of its group's stream (group =
+ * i >> group_log2, stream key mix64(key ^ GROUP_SALT)). */
+#define GROUP_SALT 0x6A09E667F3BCC909ull
+
+typedef struct {
+    int base, gshift;
+    uint64_t cmask, key, gkey;
+} orc_gen;
+
+static int orc_gen_init(int mode, uint64_t seed, orc_gen *g) {
+    unsigned w = (unsigned)mode, base = w & 0xFFu, gs = (w >> 8) & 0xFFu, c = (w >> 16) & 0xFFu;
+    if ((w >> 24) || base > 1u || gs > 40u || c > 16u) return 0;
+    uint64_t h = c ? (((1ull << c) - 1ull) << (32 - c)) : 0ull;
+    g->base = (int)base;
+    g->gshift = (int)gs;
+    g->cmask = (h << 32) | h;
+    g->key = orc_ray_key(seed, base);
+    g->gkey = mix64(g->key ^ GROUP_SALT);
+    return 1;
+}
+
+/* draw k of ray idx: mix64(s0 + (k + 1) * golden), group bits spliced in */
+static inline uint64_t orc_draw(const orc_gen *g, uint64_t s0, uint64_t gs, unsigned k) {
+    uint64_t z = mix64(s0 + (uint64_t)(k + 1) * GOLDEN);
+    if (!g->cmask) return z;
+    return (z & ~g->cmask) | (mix64(gs + (uint64_t)(k + 1) * GOLDEN) & g->cmask);
+}
+
+static void orc_raygen_gen(const orc_gen *g, const double box[4], uint64_t idx, double out[4]) {
+    uint64_t s0 = g->key ^ idx; /* per-ray SplitMix64 stream: mix64(s0 + (k + 1) * golden) */
+    uint64_t gs = g->gkey ^ (idx >> g->gshift);
     double x = 1.0, y = 0.0, r2 = 1.0;
     int ok = 0;
     for (int a = 0; a < 64; a++) {
         /* one 64-bit draw per attempt -> two 32-bit coordinates in [-1, 1) */
-        uint64_t z = mix64(s0 + (uint64_t)(a + 1) * GOLDEN);
+        uint64_t z = orc_draw(g, s0, gs, (unsigned)a);
         x = 2.0 * ((double)(uint32_t)(z >> 32) * 0x1p-32) - 1.0;
         y = 2.0 * ((double)(uint32_t)(z & 0xffffffffull) * 0x1p-32) - 1.0;
         r2 = x * x + y * y;
@@ -165,10 +196,10 @@ void orc_raygen_one(int mode, const double box[4], uint64_t key, uint64_t idx, d
     }
     double x0 = box[0], y0 = box[1], x1 = box[2], y1 = box[3];
     double W = x1 - x0, H = y1 - y0;
-    uint64_t zuv = mix64(s0 + 129 * GOLDEN); /* draw 128: u, v = its 32-bit halves * 2^-32 */
+    uint64_t zuv = orc_draw(g, s0, gs, 128u); /* draw 128: u, v = its 32-bit halves * 2^-32 */
     double u = (double)(uint32_t)(zuv >> 32) * 0x1p-32, v = (double)(uint32_t)zuv * 0x1p-32;
     double ox, oy;
-    if (mode == 1) {
+    if (g->base == 1) {
         ox = x0 + W * u;
         oy = y0 + H * v;
     } else {
@@ -185,10 +216,13 @@ void orc_raygen_one(int mode, const double box[4], uint64_t key, uint64_t idx, d
     out[0] = ox; out[1] = oy; out[2] = dx; out[3] = dy;
 }
 
-void orc_raygen(int mode, const double *box, uint64_t seed, uint64_t first, int64_t n, double *out) {
-    uint64_t key = orc_ray_key(seed, (uint64_t)mode);
+/* returns 0, or -1 for a malformed mode word */
+int orc_raygen(int mode, const double *box, uint64_t seed, uint64_t first, int64_t n, double *out) {
+    orc_gen g;
+    if (!orc_gen_init(mode, seed, &g)) return -1;
 #pragma omp parallel for schedule(static)
-    for (int64_t i = 0; i < n; i++) orc_raygen_one(mode, box, key, first + (uint64_t)i, out + 4 * i);
+    for (int64_t i = 0; i < n; i++) orc_raygen_gen(&g, box, first + (uint64_t)i, out + 4 * i);
+    return 0;
 }
 
 /* ------------------------------------------------------------------ */

@@ -53,7 +53,7 @@ def lib():
         i32, i64, u64, dbl = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_double
         L.orc_hypot.restype = dbl
         L.orc_hypot.argtypes = [dbl, dbl]
-        L.orc_raygen.restype = None
+        L.orc_raygen.restype = ctypes.c_int
         L.orc_raygen.argtypes = [ctypes.c_int, P, u64, u64, i64, P]
         L.orc_mesh_create.restype = P
         L.orc_mesh_create.argtypes = [ctypes.c_int, P, P, ctypes.c_int, P, P, P,
@@ -157,7 +157,8 @@ def hypot(x: float, y: float) -> float:
 def raygen(mode: int, box, seed: int, first: int, n: int) -> np.ndarray:
     out = np.empty((n, 4), dtype=np.float64)
     b = np.ascontiguousarray(box, dtype=np.float64)
-    lib().orc_raygen(mode, _p(b), seed, first, n, _p(out))
+    if lib().orc_raygen(mode, _p(b), seed, first, n, _p(out)) != 0:
+        raise ValueError(f"malformed ray generator mode word {mode:#x}")
     return out
 
 

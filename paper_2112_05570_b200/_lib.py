@@ -34,6 +34,15 @@ STATUS_NAMES = ("error", "fallback", "grazing", "canonical", "parallel", "zero_s
 RAYS_BOX_ENTRY = 0
 RAYS_INTERIOR = 1
 
+
+def rays_coherent(base: int, group_log2: int = 9, cell_bits: int = 12) -> int:
+    """MWT_RAYS_COHERENT(base, group_log2, cell_bits) of include/mwt.h."""
+    return base | (group_log2 << 8) | (cell_bits << 16)
+
+
+RAYS_BOX_ENTRY_COHERENT = rays_coherent(RAYS_BOX_ENTRY)  # MWT_RAYS_BOX_ENTRY_COHERENT
+RAYS_INTERIOR_COHERENT = rays_coherent(RAYS_INTERIOR)
+
 HIST_STEP_BINS = 1024
 HIST_HIT = 1024
 HIST_MISS = 1025
@@ -63,6 +72,7 @@ SIGNATURES = {
     "mwt_abi_version": (INT, []),
     "mwt_last_error": (ctypes.c_char_p, []),
     "mwt_device_count": (INT, [P]),
+    "mwt_probe_l2_read": (INT, [INT, I64, INT, P]),
     "mwt_set_tuning": (INT, [INT, INT, INT]),
     "mwt_mesh_create": (INT, [P, P, I32, P, P, P, I32, P, P, I32, INT, P]),
     "mwt_mesh_destroy": (INT, [P]),

@@ -19,6 +19,14 @@ int fail(int code, const std::string &msg) {
     return code;
 }
 
+// a generator mode word of include/mwt.h: base mode, group_log2 <= 40, cell_bits <= 16
+bool mode_ok(int mode) {
+    const unsigned w = (unsigned)mode;
+    const unsigned base = w & 0xFFu, gs = (w >> 8) & 0xFFu, c = (w >> 16) & 0xFFu;
+    return (w >> 24) == 0u && (base == MWT_RAYS_BOX_ENTRY || base == MWT_RAYS_INTERIOR) && gs <= 40u &&
+           c <= 16u;
+}
+
 int cuda_fail(cudaError_t e, const char *where) {
     g_err = std::string(where) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
     return MWT_E_CUDA;
@@ -98,6 +106,18 @@ int mwt_set_tuning(int refill_below, int min_blocks_per_sm, int variant) {
 }
 
 const char *mwt_last_error(void) { return g_err.c_str(); }
+
+int mwt_probe_l2_read(int device, int64_t bytes, int passes, double *gbs_out) {
+    if (!gbs_out || bytes < (1 << 20) || bytes > (int64_t(1) << 30) || passes < 1 || passes > 100000)
+        return fail(MWT_E_INVALID, "probe_l2_read: bad argument");
+    DeviceGuard g(device);
+    if (!g.ok) return fail(MWT_E_INVALID, "probe_l2_read: bad device");
+    float ms = 0.f;
+    int rc = mwt::probe_l2_read((size_t)bytes, passes, &ms);
+    if (rc) return cuda_fail((cudaError_t)rc, "probe_l2_read");
+    *gbs_out = (double)bytes * passes / (ms * 1e-3) / 1e9;
+    return MWT_OK;
+}
 
 int mwt_device_count(int *count) {
     if (!count) return fail(MWT_E_INVALID, "device_count: NULL");
@@ -279,7 +299,7 @@ int mwt_mesh_anchors(const mwt_mesh *m, int32_t *out_host) {
 
 int mwt_raygen_dev(int mode, const double *box, uint64_t seed, uint64_t first, int64_t n,
                    double *rays_out, void *stream) {
-    if (!box || (n > 0 && !rays_out) || n < 0 || (mode != MWT_RAYS_BOX_ENTRY && mode != MWT_RAYS_INTERIOR))
+    if (!box || (n > 0 && !rays_out) || n < 0 || !mode_ok(mode))
         return fail(MWT_E_INVALID, "raygen: bad argument");
     int rc = mwt::launch_raygen(mode, box, seed, first, n, rays_out, stream);
     if (rc) return cuda_fail((cudaError_t)rc, "raygen launch");
@@ -396,7 +416,7 @@ int mwt_trace_host(const mwt_mesh *cm, const double *rays, const int32_t *start,
 int mwt_trace_generated_dev(const mwt_mesh *m, int mode, const double *box, uint64_t seed,
                             uint64_t first, int64_t n, int32_t *out_seg, double *out_t,
                             int32_t *out_steps, int64_t *hist, void *stream) {
-    if (!m || !box || n < 0 || (mode != MWT_RAYS_BOX_ENTRY && mode != MWT_RAYS_INTERIOR))
+    if (!m || !box || n < 0 || !mode_ok(mode))
         return fail(MWT_E_INVALID, "trace_generated: bad argument");
     if (m->dev.nt == 0) return fail(MWT_E_INVALID, "trace_generated: mesh has no triangles");
     DeviceGuard g(m->device);
@@ -609,7 +629,7 @@ int shard_args_ok(const mwt_mesh *const *meshes, int ndev) {
 int mwt_trace_generated_sharded(const mwt_mesh *const *meshes, int ndev, int mode, const double *box,
                                 uint64_t seed, uint64_t first, int64_t n, int64_t *hist_out) {
     if (!shard_args_ok(meshes, ndev) || !box || n < 0 || !hist_out ||
-        (mode != MWT_RAYS_BOX_ENTRY && mode != MWT_RAYS_INTERIOR))
+        !mode_ok(mode))
         return fail(MWT_E_INVALID, "trace_generated_sharded: bad argument");
     std::vector<std::vector<int64_t>> part(ndev, std::vector<int64_t>(MWT_HIST_LEN, 0));
     std::vector<ShardErr> err(ndev);

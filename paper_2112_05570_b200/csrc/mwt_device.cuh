@@ -158,11 +158,55 @@ __host__ __device__ __forceinline__ unsigned long long mix64(unsigned long long 
 static inline unsigned long long ray_key(unsigned long long seed, unsigned long long stream) {
     return mix64(mix64(seed + kGolden) ^ (stream * 0xD1B54A32D192ED03ull));
 }
+constexpr unsigned long long kGroupSalt = 0x6A09E667F3BCC909ull;
+
+struct Box {
+    double x0, y0, x1, y1;
+};
+
+// A generator specification (mode word of include/mwt.h, decoded on the host).
+// Coherent mode (cmask != 0): every 64-bit draw k of ray i has the top c bits
+// of each 32-bit half replaced by draw k of its group's stream (group =
+// i >> gshift).  Each ray's draws stay uniform 64-bit words (bits from two
+// independent uniform streams), so every ray has exactly the iid
+// distribution; rays of one group share a cell of the disk-rejection square
+// (direction) and of the side / position draw (entry point).
+struct RayGen {
+    int mode;  // MWT_RAYS_BOX_ENTRY / MWT_RAYS_INTERIOR
+    int gshift;
+    unsigned long long cmask;  // 0: iid
+    Box box;
+    unsigned long long key, gkey;
+};
+
+// decode an include/mwt.h mode word; false if malformed
+static inline bool make_raygen(int mode_word, const double *box, unsigned long long seed, RayGen &g) {
+    const unsigned w = (unsigned)mode_word;
+    const int base = (int)(w & 0xFFu), gs = (int)((w >> 8) & 0xFFu), c = (int)((w >> 16) & 0xFFu);
+    if ((w >> 24) != 0u || (base != MWT_RAYS_BOX_ENTRY && base != MWT_RAYS_INTERIOR) || gs > 40 || c > 16)
+        return false;
+    g.mode = base;
+    g.gshift = gs;
+    const unsigned long long h = c ? (((1ull << c) - 1ull) << (32 - c)) : 0ull;
+    g.cmask = (h << 32) | h;
+    g.box = Box{box[0], box[1], box[2], box[3]};
+    g.key = ray_key(seed, (unsigned long long)base);
+    g.gkey = mix64(g.key ^ kGroupSalt);
+    return true;
+}
+
+// draw k (0-based) of a ray: mix64(s0 + (k + 1) * golden), group bits spliced in
+__device__ __forceinline__ unsigned long long draw(const RayGen &g, unsigned long long s0,
+                                                   unsigned long long gs, unsigned k) {
+    const unsigned long long z = mix64(s0 + (unsigned long long)(k + 1) * kGolden);
+    if (!g.cmask) return z;
+    return (z & ~g.cmask) | (mix64(gs + (unsigned long long)(k + 1) * kGolden) & g.cmask);
+}
 
 // rejection attempt a: one 64-bit draw -> two 32-bit coordinates in [-1, 1)
-__device__ __forceinline__ void disk_try(unsigned long long s0, int a, double &x, double &y,
-                                         double &r2) {
-    const unsigned long long z = mix64(s0 + (unsigned long long)(a + 1) * kGolden);
+__device__ __forceinline__ void disk_try(const RayGen &g, unsigned long long s0, unsigned long long gs,
+                                         int a, double &x, double &y, double &r2) {
+    const unsigned long long z = draw(g, s0, gs, (unsigned)a);
     // x = 2 * (hi * 2^-32) - 1, built without an integer conversion: the double
     // 2 + hi * 2^-31 has hi in its top mantissa bits, and subtracting 3 is exact
     // (both forms are exact, so the bits agree with the host twins)
@@ -172,26 +216,23 @@ __device__ __forceinline__ void disk_try(unsigned long long s0, int a, double &x
     r2 = x * x + y * y;
 }
 
-struct Box {
-    double x0, y0, x1, y1;
-};
-
-__device__ __forceinline__ Ray gen_ray(int mode, const Box &b, unsigned long long key,
-                                       unsigned long long idx) {
+__device__ __forceinline__ Ray gen_ray(const RayGen &g, unsigned long long idx) {
     // per-ray SplitMix64 stream: draws mix64(s0 + (k + 1) * golden), s0 = key ^ index
-    const unsigned long long s0 = key ^ idx;
+    const unsigned long long s0 = g.key ^ idx;
+    const unsigned long long gs = g.gkey ^ (idx >> g.gshift);  // the group's stream
+    const Box &b = g.box;
     // unit-disk rejection: the first accepted attempt a in 0..63.  Attempts 0
     // and 1 are evaluated unconditionally (accepted together with probability
     // 1 - (1 - pi/4)^2 = 95%) so the warp stays converged; the rest is a rare loop.
     double xa, ya, ra, xb, yb, rb;
-    disk_try(s0, 0, xa, ya, ra);
-    disk_try(s0, 1, xb, yb, rb);
+    disk_try(g, s0, gs, 0, xa, ya, ra);
+    disk_try(g, s0, gs, 1, xb, yb, rb);
     const bool oka = ra <= 1.0 && ra > 0x1p-60, okb = rb <= 1.0 && rb > 0x1p-60;
     double x = oka ? xa : xb, y = oka ? ya : yb, r2 = oka ? ra : rb;
     bool ok = oka || okb;
     if (!ok) {
         for (int a = 2; a < 64; a++) {
-            disk_try(s0, a, x, y, r2);
+            disk_try(g, s0, gs, a, x, y, r2);
             if (r2 <= 1.0 && r2 > 0x1p-60) {
                 ok = true;
                 break;
@@ -210,11 +251,11 @@ __device__ __forceinline__ Ray gen_ray(int mode, const Box &b, unsigned long lon
     const double W = b.x1 - b.x0, H = b.y1 - b.y0;
     // u, v: the two 32-bit halves of draw 128 (hi * 2^-32, lo * 2^-32), built
     // as 1 + h * 2^-32 - 1 (exact)
-    const unsigned long long zuv = mix64(s0 + 129ull * kGolden);
+    const unsigned long long zuv = draw(g, s0, gs, 128u);
     const unsigned uh = (unsigned)(zuv >> 32), vl = (unsigned)zuv;
     const double u = __hiloint2double((int)(0x3FF00000u | (uh >> 12)), (int)(uh << 20)) - 1.0;
     const double v = __hiloint2double((int)(0x3FF00000u | (vl >> 12)), (int)(vl << 20)) - 1.0;
-    if (mode == MWT_RAYS_INTERIOR) {
+    if (g.mode == MWT_RAYS_INTERIOR) {
         r.ox = b.x0 + W * u;
         r.oy = b.y0 + H * v;
     } else {

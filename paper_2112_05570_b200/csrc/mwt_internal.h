@@ -188,6 +188,9 @@ int launch_trace_generated(const MeshDev &m, int mode, const double *box, uint64
                            uint64_t first, int64_t n, int32_t *o_seg, double *o_t,
                            int32_t *o_steps, long long *hist, void *stream);
 void set_tuning(int refill_below, int min_blocks, int variant);
+// L2 read-bandwidth probe (the walk's on-chip roof, measured on the box):
+// streaming 128-bit ld.global.cg over a bytes-sized buffer, `passes` times
+int probe_l2_read(size_t bytes, int passes, float *ms);
 int launch_histogram(const int32_t *seg, const int32_t *steps, const uint32_t *st, int64_t n,
                      long long *hist, void *stream);
 int launch_bvh(const MeshDev &m, const BvhDev &b, const double *rays, int64_t n, int32_t *o_seg,

@@ -334,4 +334,53 @@ int launch_brute(const MeshDev &m, const double *rays, int64_t n, int32_t *o_seg
     MWT_LAUNCH_RET;
 }
 
+// ---------------------------------------------------------------------------
+// L2 read probe ("streaming 128-bit loads over an 8-32 MB
+// buffer, across all SMs"): the roof the bench divides the walk's algorithmic
+// bytes by, measured in the same process as the walk.
+
+__global__ void __launch_bounds__(512) k_l2_stream(const uint4 *__restrict__ p, size_t n, int passes,
+                                                   unsigned *sink) {
+    unsigned acc = 0;
+    const size_t stride = (size_t)gridDim.x * blockDim.x;
+    for (int r = 0; r < passes; r++)
+        for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+            uint4 v;
+            asm volatile("ld.global.cg.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                         : "l"(p + i));
+            acc ^= v.x ^ v.y ^ v.z ^ v.w;
+        }
+    if (acc == 0x12345678u) *sink = acc;  // keeps the loads
+}
+
+int probe_l2_read(size_t bytes, int passes, float *ms) {
+    uint4 *p = nullptr;
+    unsigned *sink = nullptr;
+    cudaEvent_t a = nullptr, b = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) e = cudaMalloc(&sink, 4);
+    if (e == cudaSuccess) e = cudaMemset(p, 1, bytes);
+    if (e == cudaSuccess) e = cudaEventCreate(&a);
+    if (e == cudaSuccess) e = cudaEventCreate(&b);
+    if (e == cudaSuccess) {
+        int dev = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const size_t n = bytes / 16;
+        k_l2_stream<<<sms * 4, 512>>>(p, n, 2, sink);  // warm: the buffer into L2
+        cudaEventRecord(a);
+        k_l2_stream<<<sms * 4, 512>>>(p, n, passes, sink);
+        cudaEventRecord(b);
+        e = cudaEventSynchronize(b);
+        if (e == cudaSuccess) e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaEventElapsedTime(ms, a, b);
+    }
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+    if (sink) cudaFree(sink);
+    if (p) cudaFree(p);
+    return (int)e;
+}
+
 }  // namespace mwt

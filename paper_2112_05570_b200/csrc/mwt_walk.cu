@@ -445,9 +445,8 @@ __device__ __forceinline__ void hist_flush(unsigned int *h, unsigned long long s
 // the persistent trace kernel
 
 struct RaySrc {
-    int mode;          // generated rays: MWT_RAYS_*
-    Box box;
-    unsigned long long key, first;
+    RayGen gen;        // generated rays (GEN == true)
+    unsigned long long first;
     const double *rays;   // loaded rays (GEN == false)
     const int32_t *start; // optional given start triangles
 };
@@ -559,11 +558,11 @@ __device__ __forceinline__ Init prologue_body(const MeshDev &M, const BTab &T, c
                                               long long i) {
     Init o;
     o.st = 0;
-    const Ray r = GEN ? gen_ray(src.mode, src.box, src.key, src.first + (unsigned long long)i)
+    const Ray r = GEN ? gen_ray(src.gen, src.first + (unsigned long long)i)
                       : load_ray(src.rays, i);
     o.ox = r.ox; o.oy = r.oy; o.dx = r.dx; o.dy = r.dy;
     // (generated interior rays never start on the box: skip the table)
-    if (!src.start && !(GEN && src.mode == MWT_RAYS_INTERIOR)) {
+    if (!src.start && !(GEN && src.gen.mode == MWT_RAYS_INTERIOR)) {
         WalkState bs;
         if (boundary_start(M, T, r, bs)) {
             o.start = bs.kr / 3;
@@ -972,12 +971,12 @@ __global__ void __launch_bounds__(THREADS, MINB)
     }
 }
 
-__global__ void __launch_bounds__(kThreads) k_raygen(int mode, Box box, unsigned long long key,
+__global__ void __launch_bounds__(kThreads) k_raygen(const __grid_constant__ RayGen g,
                                                      unsigned long long first, long long n,
                                                      double *rays) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
-        Ray r = gen_ray(mode, box, key, first + (unsigned long long)i);
+        Ray r = gen_ray(g, first + (unsigned long long)i);
         double2 *p = reinterpret_cast<double2 *>(rays) + 2 * i;
         p[0] = make_double2(r.ox, r.oy);
         p[1] = make_double2(r.dx, r.dy);
@@ -1116,9 +1115,9 @@ static void launch_k_trace_any(const MeshDev &m, const Launch &L, long long n, l
 int launch_raygen(int mode, const double *box, uint64_t seed, uint64_t first, int64_t n,
                   double *rays, void *stream) {
     if (n <= 0) return 0;
-    Box b{box[0], box[1], box[2], box[3]};
-    k_raygen<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(mode, b, ray_key(seed, mode), first,
-                                                                 n, rays);
+    RayGen g;
+    if (!make_raygen(mode, box, seed, g)) return (int)cudaErrorInvalidValue;
+    k_raygen<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(g, first, n, rays);
     MWT_LAUNCH_RET;
 }
 
@@ -1146,9 +1145,7 @@ int launch_trace_generated(const MeshDev &m, int mode, const double *box, uint64
                            int32_t *o_steps, long long *hist, void *stream) {
     if (n <= 0) return 0;
     Launch L{};
-    L.src.mode = mode;
-    L.src.box = Box{box[0], box[1], box[2], box[3]};
-    L.src.key = ray_key(seed, mode);
+    if (!make_raygen(mode, box, seed, L.src.gen)) return (int)cudaErrorInvalidValue;
     L.src.first = first;
     L.out = TraceOut{nullptr, o_seg, o_steps, o_t, nullptr, nullptr, nullptr};
     launch_k_trace_any<true>(m, L, n, hist, stream);

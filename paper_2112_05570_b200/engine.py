@@ -19,19 +19,23 @@ from ._lib import check, lib, ptr
 from .formats import SceneArrays, TriArrays, load_scene, load_structure, load_tri
 
 
-def _stream(stream=None):
-    s = torch.cuda.current_stream() if stream is None else stream
+def _stream(stream=None, device: int | None = None):
+    """The stream a call launches on: ``stream``, else the current stream of
+    the handle's own ``device`` (the C side switches to that device)."""
+    s = torch.cuda.current_stream(device) if stream is None else stream
     return ctypes_void(s.cuda_stream)
 
 
 def _held(t: torch.Tensor | None, stream=None) -> torch.Tensor | None:
-    """``t`` made contiguous; when the kernel runs on a stream other than the
-    current one, a temporary copy is kept alive for that stream's work
+    """``t`` made contiguous.  When the kernel runs on a side ``stream`` and a
+    temporary copy was needed, that stream first waits for the copy (made on
+    the current stream of t's device) and the copy is kept alive for its work
     (record_stream) so the caching allocator does not hand it out early."""
     if t is None:
         return None
     c = t.contiguous()
     if stream is not None and c.data_ptr() != t.data_ptr():
+        stream.wait_stream(torch.cuda.current_stream(t.device))
         c.record_stream(stream)
     return c
 
@@ -117,7 +121,7 @@ class DeviceMesh:
         out = torch.empty((n, 4), dtype=torch.float64, device=self._dev())
         b = _f64(box)
         check(lib.mwt_raygen_dev(int(mode), ptr(b), int(seed), int(first), int(n), ptr(out),
-                                 _stream(stream)), "raygen")
+                                 _stream(stream, self.device)), "raygen")
         return out
 
     def locate_device(self, pts: torch.Tensor, stream=None):
@@ -125,7 +129,7 @@ class DeviceMesh:
         n = pts.shape[0]
         tid = torch.empty(n, dtype=torch.int32, device=pts.device)
         st = torch.empty(n, dtype=torch.int32, device=pts.device)
-        check(lib.mwt_locate_dev(self._h, ptr(pts), n, ptr(tid), ptr(st), _stream(stream)), "locate")
+        check(lib.mwt_locate_dev(self._h, ptr(pts), n, ptr(tid), ptr(st), _stream(stream, self.device)), "locate")
         return tid, st
 
     def trace_device(self, rays: torch.Tensor, start: torch.Tensor | None = None, stream=None,
@@ -141,7 +145,7 @@ class DeviceMesh:
         g = out.get
         check(lib.mwt_trace_dev(self._h, ptr(rays), ptr(start) if start is not None else None,
                                 n, ptr(g("start")), ptr(g("seg")), ptr(g("t")), ptr(g("u")),
-                                ptr(g("steps")), ptr(g("status")), _stream(stream)), "trace")
+                                ptr(g("steps")), ptr(g("status")), _stream(stream, self.device)), "trace")
         return out
 
     def trace_chain_device(self, rays: torch.Tensor, start: torch.Tensor | None = None,
@@ -160,7 +164,7 @@ class DeviceMesh:
         check(lib.mwt_trace_chain_dev(self._h, ptr(rays),
                                       ptr(start) if start is not None else None, n,
                                       ptr(out["end"]), ptr(out["seg"]), ptr(out["t"]), ptr(out["u"]),
-                                      ptr(out["steps"]), ptr(out["status"]), _stream(stream)),
+                                      ptr(out["steps"]), ptr(out["status"]), _stream(stream, self.device)),
               "trace_chain")
         return out
 
@@ -177,7 +181,7 @@ class DeviceMesh:
         b = _f64(box)
         check(lib.mwt_trace_generated_dev(self._h, int(mode), ptr(b), int(seed), int(first), int(n),
                                           ptr(g("seg")), ptr(g("t")), ptr(g("steps")), ptr(hist),
-                                          _stream(stream)), "trace_generated")
+                                          _stream(stream, self.device)), "trace_generated")
         return out
 
     def brute_force_device(self, rays: torch.Tensor, stream=None) -> dict:
@@ -187,7 +191,7 @@ class DeviceMesh:
                    t=torch.empty(n, dtype=torch.float64, device=rays.device),
                    u=torch.empty(n, dtype=torch.float64, device=rays.device))
         check(lib.mwt_brute_force_dev(self._h, ptr(rays), n, ptr(out["seg"]), ptr(out["t"]),
-                                      ptr(out["u"]), _stream(stream)), "brute_force")
+                                      ptr(out["u"]), _stream(stream, self.device)), "brute_force")
         return out
 
     # -- host-buffer operations -------------------------------------------
@@ -271,7 +275,7 @@ class DeviceBvh:
                    status=torch.empty(n, dtype=torch.int32, device=d))
         check(lib.mwt_bvh_trace_dev(self._h, ptr(rays), n, ptr(out["seg"]), ptr(out["t"]),
                                     ptr(out["u"]), ptr(out["node_tests"]), ptr(out["prim_tests"]),
-                                    ptr(out["status"]), _stream(stream)), "bvh_trace")
+                                    ptr(out["status"]), _stream(stream, self.mesh.device)), "bvh_trace")
         return out
 
     def trace(self, rays: np.ndarray) -> dict:
@@ -331,7 +335,7 @@ class DeviceKd:
                    status=torch.empty(n, dtype=torch.int32, device=d))
         check(lib.mwt_kd_trace_dev(self._h, ptr(rays), n, ptr(out["seg"]), ptr(out["t"]),
                                    ptr(out["u"]), ptr(out["nodes"]), ptr(out["ropes"]),
-                                   ptr(out["prims"]), ptr(out["status"]), _stream(stream)), "kd_trace")
+                                   ptr(out["prims"]), ptr(out["status"]), _stream(stream, self.mesh.device)), "kd_trace")
         return out
 
     def trace(self, rays: np.ndarray) -> dict:
@@ -373,6 +377,15 @@ def trace_sharded(meshes, rays: np.ndarray, start: np.ndarray | None = None) -> 
                                      ptr(out["start"]), ptr(out["seg"]), ptr(out["t"]), ptr(out["u"]),
                                      ptr(out["steps"]), ptr(out["status"])), "trace_host_sharded")
     return out
+
+
+def probe_l2_read_gbs(device: int = 0, nbytes: int = 64 << 20, passes: int = 200) -> float:
+    """L2 read bandwidth of ``device`` (mwt_probe_l2_read): 128-bit streaming
+    loads over an L2-resident buffer -- the walk's on-chip memory roof."""
+    import ctypes
+    g = ctypes.c_double(0.0)
+    check(lib.mwt_probe_l2_read(int(device), int(nbytes), int(passes), ctypes.byref(g)), "probe_l2_read")
+    return float(g.value)
 
 
 def new_histogram(device: int = 0) -> torch.Tensor:

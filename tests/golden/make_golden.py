@@ -9,6 +9,8 @@ returns.  Outputs (committed): tests/golden/*.npz.
   struct_<c>.npz  per config: reference bvh/kd results + counters on a ray subset
   hypot.npz     math.hypot values (CPython's is correctly rounded)
   degenerate.npz  rays where the reference walk and brute force disagree
+  branches.npz  hand-built inputs forcing the walk's fallback / TraversalError /
+                parallel-exit branches and outside-the-mesh locates
 
 Usage: python tests/golden/make_golden.py [group ...]
 """
@@ -340,6 +342,168 @@ def make_degenerate():
     np.savez_compressed(os.path.join(HERE, "degenerate.npz"), **out)
 
 
+# ----------------------------------------------------------------------
+# Branches random rays never reach (accel.py:164-168, :182-191, :198 into
+# geometry.py:149-161, accel.py:241-246, :287-288), each forced by a
+# hand-built input and recorded from the reference itself.
+
+def run_walk_given(tri, rays, starts, index=None):
+    """traverse_triangulation from GIVEN start triangles; error = 1 for a
+    revisit ('traversal loop', accel.py:164-168), 2 for no exit edge
+    (accel.py:190-191)."""
+    from mintri.accel import TraversalError
+    index = index or SceneIndex(tri.scene)
+    n = len(rays)
+    out = dict(start=np.asarray(starts, np.int32).copy(), seg=np.full(n, -1, np.int32), t=np.full(n, np.nan),
+               u=np.full(n, np.nan), steps=np.zeros(n, np.int32), error=np.zeros(n, np.uint8))
+    for i, r in enumerate(rays):
+        try:
+            hit, st = traverse_triangulation(tri, r, int(starts[i]), index)
+        except TraversalError as e:
+            out["error"][i] = 1 if "loop" in str(e) else 2
+            continue
+        out["steps"][i] = st.tri_steps
+        if hit is not None:
+            out["seg"][i] = hit.seg
+            out["t"][i] = hit.t
+            seg = tri.scene.segments[hit.seg]
+            ex, ey = seg.b.x - seg.a.x, seg.b.y - seg.a.y
+            out["u"][i] = ((hit.point.x - seg.a.x) * ex + (hit.point.y - seg.a.y) * ey) / (ex * ex + ey * ey)
+    return out
+
+
+def fan_mesh(cx, cy, constrained=True):
+    """The unit square as a 4-triangle fan around a centre vertex (cx, cy), the
+    edge corner0 -> centre constrained as geometry segment 0 (or nothing
+    constrained but the square).  Moving the centre onto a side makes a
+    triangle degenerate (three collinear corners: no exit edge for a ray
+    parallel to it, accel.py:190-191); moving it outside the square inverts
+    triangles: fallback exits, and a ray whose line separates the centre from
+    the four corners circles the centre forever (revisit, accel.py:164-168)."""
+    from mintri.scene import Scene, unit_square_boundary
+    from mintri.trimesh import Triangulation
+    geo = [Segment(Point(0.0, 0.0), Point(cx, cy))] if constrained else []
+    g = len(geo)
+    sc = Scene(geo + unit_square_boundary(), name="fan")
+    tri = Triangulation(sc)
+    for x, y in ((0.0, 0.0), (1.0, 0.0), (1.0, 1.0), (0.0, 1.0), (cx, cy)):
+        tri.add_vertex(x, y, 0)
+    c = 0 if constrained else -1
+    # T0=(0,1,4) T1=(1,2,4) T2=(2,3,4) T3=(3,0,4); edge i opposite v[i]
+    tri._new_tri(0, 1, 4, nbr=[1, 3, None], flag=[-1, c, g + 0])
+    tri._new_tri(1, 2, 4, nbr=[2, 0, None], flag=[-1, -1, g + 1])
+    tri._new_tri(2, 3, 4, nbr=[3, 1, None], flag=[-1, -1, g + 2])
+    tri._new_tri(3, 0, 4, nbr=[0, 2, None], flag=[c, -1, g + 3])
+    return sc, tri
+
+
+def diagonal_chain_mesh():
+    """A diagonal segment (0.25, 0.25) -> (0.75, 0.75) whose constrained chain
+    runs through a vertex 2^-40 off its line: rays exactly parallel to the
+    segment (direction (s, s)) cross the chain edge, so ray_segment_intersect
+    takes its parallel branch at a walk exit (accel.py:198, geometry.py:149-161):
+    collinear rays hit an endpoint, offset ones fall to the grazing fallback."""
+    from mintri.scene import Scene, unit_square_boundary
+    a, b = Point(0.25, 0.25), Point(0.75, 0.75)
+    m = Point(0.5, 0.5 + 2.0 ** -40)
+    sc1 = Scene([Segment(a, m), Segment(m, b)] + unit_square_boundary(), name="chain")
+    tri = build_cdt(sc1)
+    sc2 = Scene([Segment(a, b)] + unit_square_boundary(), name="diagonal")
+    remap = {0: 0, 1: 0, 2: 1, 3: 2, 4: 3, 5: 4}
+    for tid in tri.alive_tris():
+        t = tri.tris[tid]
+        t.flag = [f if f == -1 else remap[f] for f in t.flag]
+    tri.scene = sc2
+    with tempfile.TemporaryDirectory() as d:
+        p = os.path.join(d, "t.tri")
+        save_triangulation(tri, p)
+        return sc2, load_triangulation(p, sc2)
+
+
+def make_branches():
+    import warnings
+    out = {}
+    names = []
+    rng = np.random.default_rng(7)
+
+    def record(name, sc, tri, rays, starts=None, loc_pts=None):
+        xy, kind = scene_arrays(sc)
+        vxy, v, nbr, flag = tri_arrays(tri)
+        d = dict(seg_xy=xy, seg_kind=kind, vxy=vxy, v=v, nbr=nbr, flag=flag, rays=ray_arr(rays))
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")  # locate_brute_force's "outside all triangles"
+            if starts is None:
+                loc = TriLocator(tri)
+                starts = [loc.locate(r.origin) for r in rays]
+            d.update(prefixed("w_", run_walk_given(tri, rays, starts)))
+            if loc_pts is not None:
+                loc = TriLocator(tri)
+                d["loc_pts"] = np.array(loc_pts, np.float64).reshape(-1, 2)
+                d["loc_anchor"] = np.array([loc.locate(Point(*p)) for p in loc_pts], np.int32)
+                d["loc_brute"] = np.array([locate_triangle(tri, Point(*p), "brute") for p in loc_pts], np.int32)
+        out.update(prefixed(f"{name}__", d))
+        names.append(name)
+        e = d["w_error"]
+        print(f"branches/{name}: {len(rays)} rays, loop errors {int((e == 1).sum())}, "
+              f"no-exit errors {int((e == 2).sum())}, hits {int((d['w_seg'] >= 0).sum())}", flush=True)
+
+    # (1) wrong start triangles on real meshes: the first triangle does not hold
+    # the origin, so exits come from the fallback rule (accel.py:182-184, :188-189)
+    for cfg, which in (("lines64", "mwt"), ("lines1024", "cdt")):
+        d = os.path.join(FIX, cfg)
+        scene = Scene.load(os.path.join(d, "scene.txt"))
+        tri = load_triangulation(os.path.join(d, f"{which}.tri"), scene)
+        arr = raygen(1, (0.0, 0.0, 1.0, 1.0), 101, 0, 3000)
+        starts = rng.integers(0, tri.num_tris, len(arr))
+        record(f"wrongstart_{cfg}_{which}", scene, tri, rays_from(arr), starts=starts)
+
+    # (2) fans: degenerate and inverted triangles -> no-exit and loop errors
+    fans = [(0.3, 0.6, True), (0.5, 0.0, True), (0.5, -0.3, True), (1.4, 0.5, True), (0.5, 1.0, True),
+            (0.5, -0.3, False), (1.4, 0.5, False), (-0.25, 0.7, False)]
+    for k, (cx, cy, con) in enumerate(fans):
+        sc, tri = fan_mesh(cx, cy, con)
+        arr = raygen(1, (-0.5, -0.5, 1.5, 1.5), 200 + k, 0, 300)
+        rays = rays_from(arr)
+        extra = [Ray(Point(x, y), Point(dx, 0.0)) for y in (0.0, cy, 1.0) for x in (-0.2, 0.1, 0.5, 0.7, 1.2)
+                 for dx in (1.0, -1.0)]
+        extra += [Ray(Point(cx, y), Point(0.0, dy)) for y in (-0.3, 0.2, 0.8) for dy in (1.0, -1.0)]
+        # lines between the centre and the square (a displaced centre: circling rays)
+        for f in (0.3, 0.5, 0.7):
+            if cy < 0.0 or cy > 1.0:
+                yy = (0.0 if cy < 0.0 else 1.0) * (1 - f) + cy * f
+                extra += [Ray(Point(x, yy), Point(dx, 0.0)) for x in (0.2, 0.5, 0.9) for dx in (1.0, -1.0)]
+            if cx < 0.0 or cx > 1.0:
+                xx = (0.0 if cx < 0.0 else 1.0) * (1 - f) + cx * f
+                extra += [Ray(Point(xx, y), Point(0.0, dy)) for y in (0.2, 0.5, 0.9) for dy in (1.0, -1.0)]
+        rays = rays + extra
+        starts = np.arange(len(rays) * 4, dtype=np.int32) % 4
+        rays4 = [r for r in rays for _ in range(4)]
+        record(f"fan{k}", sc, tri, rays4, starts=starts)
+
+    # (3) parallel branch at a constrained exit
+    sc, tri = diagonal_chain_mesh()
+    s = math.sqrt(0.5)
+    rays = []
+    for delta in (0.0, 2.0 ** -50, 2.0 ** -45, 2.0 ** -42, 2.0 ** -41, 3 * 2.0 ** -42, -2.0 ** -45, -2.0 ** -42):
+        for t0 in (0.05, 0.3, 0.45, 0.55, 0.6):
+            rays.append(Ray(Point(t0, t0 + delta), Point(s, s)))
+            rays.append(Ray(Point(1.0 - t0, 1.0 - t0 + delta), Point(-s, -s)))
+    record("parallel_exit", sc, tri, rays)
+
+    # (4) locate outside every triangle: anchor walk fails, brute force finds
+    # nothing, nearest centroid by math.hypot (accel.py:241-246, :287-288)
+    pts = [(x, y) for x in (-6.0, -0.7, -1e-9, 0.4, 1.0 + 1e-9, 1.3, 5.0) for y in (-3.0, -0.2, 0.6, 1.5, 7.0)
+           if not (0.0 <= x <= 1.0 and 0.0 <= y <= 1.0)]
+    for cfg in ("lines64", "floorplan64"):
+        d = os.path.join(FIX, cfg)
+        scene = Scene.load(os.path.join(d, "scene.txt"))
+        tri = load_triangulation(os.path.join(d, "mwt.tri"), scene)
+        arr = raygen(1, (-0.5, -0.5, 1.5, 1.5), 300, 0, 120 if cfg == "floorplan64" else 400)
+        record(f"outside_{cfg}", scene, tri, rays_from(arr), loc_pts=pts)
+    out["cases"] = np.array(names)
+    np.savez_compressed(os.path.join(HERE, "branches.npz"), **out)
+
+
 if __name__ == "__main__":
     groups = sys.argv[1:] or ["known", "hypot"] + [f"config:{c}" for c in CONFIGS] + \
         [f"struct:{c}" for c in CONFIGS[1:]]
@@ -352,6 +516,8 @@ if __name__ == "__main__":
             make_experiment()
         elif g == "degenerate":
             make_degenerate()
+        elif g == "branches":
+            make_branches()
         elif g.startswith("config:"):
             make_config(g.split(":", 1)[1])
         elif g.startswith("struct:"):

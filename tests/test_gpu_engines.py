@@ -83,7 +83,8 @@ def test_generated_kernel_equals_explicit_rays_and_histogram(cfg):
     paths = fixture_paths(cfg, "mwt") or fixture_paths(cfg, "cdt")
     m = DeviceMesh.from_files(*paths)
     n = 1 << 18
-    for mode in (0, 1):
+    from oracle import raygen as rg
+    for mode in (0, 1, rg.coherent(0), rg.coherent(1)):
         h = new_histogram()
         gen = m.trace_generated_device(mode, (0, 0, 1, 1), 3, 777, n, outputs=True, hist=h)
         rays = m.raygen_device(mode, (0, 0, 1, 1), 3, 777, n)

@@ -25,7 +25,8 @@ def test_hypot_is_cpython_hypot():
     assert np.array_equal(got.view(np.uint64), g["h"].view(np.uint64))
 
 
-@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("mode", [0, 1, rg.coherent(0), rg.coherent(1), rg.coherent(0, 0, 16),
+                                  rg.coherent(1, 40, 1)])
 def test_raygen_twins_agree(mode):
     box = (0.0, 0.0, 1.0, 0.5)
     a = rg.raygen(mode, box, 11, 1000, 50000)
@@ -34,9 +35,54 @@ def test_raygen_twins_agree(mode):
     # reference Ray would not renormalise (geometry.py:73)
     n = np.hypot(a[:, 2], a[:, 3])
     assert np.abs(n - 1.0).max() <= 1e-12
-    if mode == 0:  # origin exactly on the entered side of the box
+    if mode & 0xFF == 0:  # origin exactly on the entered side of the box
         on = (a[:, 0] == 0.0) | (a[:, 0] == 1.0) | (a[:, 1] == 0.0) | (a[:, 1] == 0.5)
         assert on.all()
+
+
+def test_raygen_mode_words():
+    """include/mwt.h MWT_RAYS_COHERENT: malformed words are rejected by every twin;
+    cell_bits 0 is the iid generator whatever the group size."""
+    for bad in (2, 0xFF, rg.coherent(0, 41, 1), rg.coherent(0, 7, 17), 1 << 24, -1):
+        with pytest.raises(ValueError):
+            rg.raygen(bad, (0, 0, 1, 1), 0, 0, 4)
+        with pytest.raises(ValueError):
+            orc.raygen(bad, (0, 0, 1, 1), 0, 0, 4)
+    a = rg.raygen(rg.coherent(0, 7, 0), (0, 0, 1, 1), 5, 3, 1000)
+    assert np.array_equal(a.view(np.uint64), rg.raygen(0, (0, 0, 1, 1), 5, 3, 1000).view(np.uint64))
+
+
+@pytest.mark.parametrize("base", [0, 1])
+def test_coherent_rays_keep_the_iid_distribution(base):
+    """Each coherent ray is an exact draw of the base distribution: the rays at
+    one position j of every group (independent groups) pass the same isotropy,
+    uniform-offset / uniform-origin tests as the iid generator; and a group's
+    rays share a cell (nearly the same line)."""
+    from scipy.stats import chisquare, kstest
+    box = (0.0, 0.0, 1.0, 0.5)
+    mode = rg.coherent(base)
+    n = 512 * 5000
+    r = rg.raygen(mode, box, 21, 0, n).reshape(-1, 512, 4)
+    for j in (0, 77, 300):
+        s = r[:, j]
+        ang = np.arctan2(s[:, 3], s[:, 2])
+        counts, _ = np.histogram(ang, bins=36, range=(-np.pi, np.pi))
+        assert chisquare(counts).pvalue > 1e-4
+        if base == 1:
+            assert kstest(s[:, 0], "uniform").pvalue > 1e-4
+            assert kstest(s[:, 1] / 0.5, "uniform").pvalue > 1e-4
+        else:
+            nx, ny = -s[:, 3], s[:, 2]
+            cx = np.array([0.0, 1.0, 1.0, 0.0])
+            cy = np.array([0.0, 0.0, 0.5, 0.5])
+            proj = nx[:, None] * cx[None, :] + ny[:, None] * cy[None, :]
+            a, b = proj.min(1), proj.max(1)
+            off = (nx * s[:, 0] + ny * s[:, 1] - a) / (b - a)
+            assert kstest(off, "uniform").pvalue > 1e-4
+    # coherence: most groups span a small angle
+    ang = np.arctan2(r[..., 3], r[..., 2])
+    spread = np.abs(np.angle(np.exp(1j * (ang - ang[:, :1])))).max(1)
+    assert np.median(spread) < 0.02
 
 
 def test_raygen_isotropic():
@@ -209,3 +255,50 @@ def test_degenerate_rays_reference_walk_not_brute_force():
         assert bf["t"][0] == g[f"{k}_brute"][1]
         k += 1
     assert k > 0
+
+
+def _branch_cases():
+    p = os.path.join(GOLDEN, "branches.npz")
+    return [str(c) for c in np.load(p)["cases"]] if os.path.exists(p) else []
+
+
+# cases whose starts the reference located itself (TriLocator); the others
+# are given start triangles (wrong starts, tangled fans)
+LOCATED = ("parallel_exit", "outside_")
+
+
+@pytest.mark.parametrize("name", _branch_cases())
+def test_branch_fixtures(name):
+    """Hand-built inputs forcing the branches random rays never reach (make_golden.py
+    make_branches): the oracle reproduces the reference's recorded outcomes,
+    TraversalError (both kinds) exactly on the reference's rays."""
+    g = _golden("branches.npz")
+    m = known_mesh(g, name)
+    rays = g[f"{name}__rays"]
+    ref = {k[len(name) + 4:]: g[k] for k in g.files if k.startswith(f"{name}__w_")}
+    out = m.trace(rays, None if name.startswith(LOCATED) else ref["start"])
+    check_walk(out, ref)
+    hit = (ref["error"] == 0) & (ref["seg"] >= 0)
+    # the reference returns the hit point, not u: its u is recovered from the point
+    assert np.all(np.abs(out["u"][hit] - ref["u"][hit]) <= 1e-9 * np.maximum(1.0, np.abs(ref["u"][hit])))
+    if f"{name}__loc_pts" in g.files:
+        tid, st = m.locate(g[f"{name}__loc_pts"])
+        assert np.array_equal(tid, g[f"{name}__loc_anchor"])
+        assert np.array_equal(tid, g[f"{name}__loc_brute"])
+        assert (st & orc.ST_LOC_OUTSIDE).all()  # every point is outside the mesh
+
+
+def test_branch_fixtures_reach_every_branch():
+    """Across the branch fixtures the reference raised both TraversalError kinds
+    and the oracle took the fallback exit, the parallel branch at a constrained
+    exit, the grazing fallback and the outside-the-mesh locate."""
+    g = _golden("branches.npz")
+    err = np.concatenate([g[f"{c}__w_error"] for c in _branch_cases()])
+    assert (err == 1).sum() > 0 and (err == 2).sum() > 0
+    bits = 0
+    for name in _branch_cases():
+        ref_start = None if name.startswith(LOCATED) else g[f"{name}__w_start"]
+        bits |= int(np.bitwise_or.reduce(known_mesh(g, name).trace(g[f"{name}__rays"], ref_start)["status"]))
+    for b in (orc.ST_ERROR, orc.ST_FALLBACK, orc.ST_PARALLEL, orc.ST_GRAZING, orc.ST_ZERO_SIDE,
+              orc.ST_LOC_OUTSIDE, orc.ST_LOC_BRUTE, orc.ST_MULTI, orc.ST_LOC_TIE):
+        assert bits & b, f"status bit {b} never set"
