@@ -33,7 +33,7 @@
 extern "C" {
 #endif
 
-#define MWT_ABI_VERSION 2
+#define MWT_ABI_VERSION 3
 
 /* return codes */
 #define MWT_OK 0
@@ -157,6 +157,11 @@ int mwt_raygen_dev(int mode, const double *box, uint64_t seed, uint64_t first, i
  *   (accel.py:284-289, :333-353).  pts = n (x, y) pairs (device). */
 int mwt_locate_dev(const mwt_mesh *mesh, const double *pts, int64_t n, int32_t *out_tid,
                    uint32_t *out_status, void *stream);
+/* Replaces: locate_triangle(tri, p, method="brute") (accel.py:341-349): the
+ * lowest triangle id that _contains p (a scan in id order), else the nearest
+ * centroid (locate_brute_force, accel.py:241-253).  O(triangles) per point. */
+int mwt_locate_brute_dev(const mwt_mesh *mesh, const double *pts, int64_t n, int32_t *out_tid,
+                         uint32_t *out_status, void *stream);
 
 /* K4 -- the MWT walk.
  * Replaces: traverse_triangulation(tri, ray, start_tri, index) (accel.py:138-213),
@@ -215,9 +220,13 @@ int mwt_kd_create(const mwt_mesh *mesh, int32_t nnodes, int32_t num_leaves, cons
                   const int32_t *ropes, const int32_t *rope_cost, const int32_t *prim_off,
                   const int32_t *prim_cnt, int32_t nprims, const int32_t *prims, mwt_kd **out);
 int mwt_kd_destroy(mwt_kd *kd);
-int mwt_kd_trace_dev(const mwt_kd *kd, const double *rays, int64_t n, int32_t *out_seg,
-                     double *out_t, double *out_u, int32_t *out_nodes, int32_t *out_rope_steps,
-                     int32_t *out_prim_tests, uint32_t *out_status, void *stream);
+/* start_leaf: NULL (locate_leaf per ray) or per-ray node indices of the
+ * leaves to start from -- kd_intersect(kd, ray, start_leaf=...) (accel.py:761-771);
+ * an index that is not a leaf gives MWT_ST_ERROR for that ray. */
+int mwt_kd_trace_dev(const mwt_kd *kd, const double *rays, const int32_t *start_leaf, int64_t n,
+                     int32_t *out_seg, double *out_t, double *out_u, int32_t *out_nodes,
+                     int32_t *out_rope_steps, int32_t *out_prim_tests, uint32_t *out_status,
+                     void *stream);
 
 /* Brute-force closest hit (the reference's oracle engine).
  * Replaces: brute_force_closest(scene, ray, index) (accel.py:101-132). */

@@ -50,7 +50,7 @@ HIST_STEPS_SUM = 1026
 HIST_STATUS0 = 1027
 HIST_LEN = 1040
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class MwtError(RuntimeError):
@@ -81,6 +81,7 @@ SIGNATURES = {
     "mwt_mesh_anchors": (INT, [P, P]),
     "mwt_raygen_dev": (INT, [INT, P, U64, U64, I64, P, P]),
     "mwt_locate_dev": (INT, [P, P, I64, P, P, P]),
+    "mwt_locate_brute_dev": (INT, [P, P, I64, P, P, P]),
     "mwt_trace_dev": (INT, [P, P, P, I64, P, P, P, P, P, P, P]),
     "mwt_trace_chain_dev": (INT, [P, P, P, I64, P, P, P, P, P, P, P]),
     "mwt_trace_host": (INT, [P, P, P, I64, P, P, P, P, P, P]),
@@ -91,7 +92,7 @@ SIGNATURES = {
     "mwt_bvh_trace_dev": (INT, [P, P, I64, P, P, P, P, P, P, P]),
     "mwt_kd_create": (INT, [P, I32, I32, P, P, P, P, P, P, P, P, P, I32, P, P]),
     "mwt_kd_destroy": (INT, [P]),
-    "mwt_kd_trace_dev": (INT, [P, P, I64, P, P, P, P, P, P, P, P]),
+    "mwt_kd_trace_dev": (INT, [P, P, P, I64, P, P, P, P, P, P, P, P]),
     "mwt_brute_force_dev": (INT, [P, P, I64, P, P, P, P]),
     "mwt_trace_generated_sharded": (INT, [P, INT, INT, P, U64, U64, I64, P]),
     "mwt_trace_host_sharded": (INT, [P, INT, P, P, I64, P, P, P, P, P, P]),

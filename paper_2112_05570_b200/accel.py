@@ -114,6 +114,11 @@ class _IdCache:
         got = self._d.get(id(obj))
         return got[1] if got is not None and got[0]() is obj else None
 
+    def pop(self, obj):
+        got = self._d.get(id(obj))
+        if got is not None and got[0]() is obj:
+            del self._d[id(obj)]
+
     def __setitem__(self, obj, value):
         key = id(obj)
         self._d[key] = (weakref.ref(obj), value)
@@ -139,17 +144,49 @@ def _segments_of(scene) -> list:
     return list(scene.segments)
 
 
+# The reference edits triangulations in place (trimesh.flip_edge, the
+# annealer's vertex moves) and its walk reads the live mesh, so a cached pack
+# is reused only while the mesh's content is unchanged: every call compares a
+# fingerprint of the vertex coordinates, triangle corners, neighbours, flags
+# and the scene's segments (O(triangles) host work).  Set CHECK_MUTATION =
+# False for meshes known to be immutable, or call invalidate(tri) after an edit.
+CHECK_MUTATION = True
+
+
+def _fingerprint(tri) -> bytes:
+    import hashlib
+    h = hashlib.blake2b(digest_size=16)
+    h.update(np.array([(v.x, v.y) for v in tri.verts], dtype=np.float64).tobytes())
+    h.update(np.array([(-1,) * 9 if t is None else
+                       (*t.v, *[-1 if n is None else n for n in t.nbr], *t.flag) for t in tri.tris],
+                      dtype=np.int64).tobytes())
+    segs = tri.scene.segments
+    h.update(np.array([(s.a.x, s.a.y, s.b.x, s.b.y) for s in segs], dtype=np.float64).tobytes())
+    h.update(bytes(_kind(s) == "G" for s in segs))
+    return h.digest()
+
+
+def invalidate(obj) -> None:
+    """Drop the cached device copy of a triangulation (or structure / scene)."""
+    for c in (_mesh_cache, _struct_cache, _scene_mesh_cache):
+        c.pop(obj)
+
+
 def pack(tri, device: int = 0) -> _Packed:
-    """Packed device mesh for a reference Triangulation (cached) or for a
-    (SceneArrays, TriArrays) pair."""
+    """Packed device mesh for a reference Triangulation (cached while its
+    content is unchanged) or for a (SceneArrays, TriArrays) pair."""
     if isinstance(tri, tuple):
         scene, arrays = tri
         return _Packed(DeviceMesh(scene_arrays(scene), arrays, device), None, scene)
     got = _mesh_cache.get(tri)
+    fp = _fingerprint(tri) if CHECK_MUTATION else None
+    if got is not None and (got.device != device or (fp is not None and got.fp != fp)):
+        got = None  # edited since it was packed (or another device): repack
     if got is None:
         tmap = _TriMap(tri)
         mesh = DeviceMesh(scene_arrays(tri.scene), tmap.arrays, device)
         got = _Packed(mesh, tmap, tri.scene)
+        got.fp, got.device = fp, device
         _mesh_cache[tri] = got
     return got
 
@@ -212,15 +249,24 @@ def traverse_triangulation(tri, ray: Ray, start_tri: int, index=None
 
 
 class TriLocator:
-    """accel.py:256-289: anchor grid of max(2, int(sqrt(T/2))) cells, walk,
-    brute-force fallback, lowest-id tie flood -- all on the device."""
+    """accel.py:256-289: anchor grid, walk, brute-force fallback, lowest-id tie
+    flood -- all on the device.
+
+    ``resolution`` (accel.py:263-268) sets the reference's anchor grid, which
+    only chooses where its walk starts: the answer is the lowest id over the
+    neighbour-connected triangles containing p, the same from any containing
+    seed.  The device seeds its search from its own finer grid (the packer's
+    cell-centre triangles), so every resolution gives the reference's result;
+    ``res`` keeps the value asked for."""
 
     def __init__(self, tri, resolution: Optional[int] = None):
         self.tri = tri
-        P = pack(tri)
-        if resolution is not None and resolution != P.mesh.info.anchor_res:
-            raise NotImplementedError("custom anchor resolution is not supported by the packer")
-        self.res = P.mesh.info.anchor_res
+        pack(tri)
+        if resolution is None:
+            resolution = max(2, int(math.sqrt(max(_num_tris(tri), 4) / 2.0)))
+        if int(resolution) < 1:
+            raise ValueError("resolution must be positive")
+        self.res = int(resolution)
 
     def locate(self, p: Point) -> int:
         tid, _ = locate_batch(self.tri, [[p[0], p[1]]])
@@ -230,16 +276,26 @@ class TriLocator:
         return locate_batch(self.tri, pts)[0]
 
 
+def _num_tris(tri) -> int:
+    n = getattr(tri, "num_tris", None)
+    return int(n) if n is not None else sum(1 for t in tri.tris if t is not None)
+
+
 def locate_triangle(tri, p: Point, method: str = "anchor",
                     locator: Optional[TriLocator] = None) -> int:
-    """accel.py:333-353.  Both methods return the lowest id among the
-    neighbour-connected triangles containing p; on the device both run the
-    anchor walk (the brute-force scan is its fallback)."""
-    if method not in ("brute", "anchor"):
-        raise ValueError(f"unknown location method {method!r}")
-    if locator is None:
-        locator = TriLocator(tri)
-    return locator.locate(p)
+    """accel.py:333-353.  "anchor": TriLocator.locate on the device; "brute":
+    the lowest triangle id containing p (a device scan in id order), else the
+    nearest centroid (mwt_locate_brute_dev)."""
+    if method == "brute":
+        P = pack(tri)
+        tid, _ = P.mesh.locate(np.array([[p[0], p[1]]], dtype=np.float64), method="brute")
+        t = int(tid[0])
+        return int(P.tmap.to_ref[t]) if P.tmap is not None else t
+    if method == "anchor":
+        if locator is None:
+            locator = TriLocator(tri)
+        return locator.locate(p)
+    raise ValueError(f"unknown location method {method!r}")
 
 
 # -- BVH / kd-tree -------------------------------------------------------
@@ -306,7 +362,7 @@ def flatten_kd(kd) -> dict:
     return dict(c_t=np.float64(getattr(kd, "c_t", np.nan)), num_leaves=np.int64(len(kd._leaves)),
                 axis=axis, pos=pos, left=left, right=right, box=box, ropes=ropes,
                 rope_counts=counts, rope_cost=cost, prim_off=poff, prim_cnt=pcnt,
-                prims=np.array(prims, np.int32))
+                prims=np.array(prims, np.int32), _node_index=index)
 
 
 _struct_cache = _IdCache()
@@ -326,7 +382,10 @@ def _device_struct(obj):
     if got is None:
         mesh = _scene_mesh(obj.scene)
         if hasattr(obj, "_leaves"):
-            got = DeviceKd(mesh, flatten_kd(obj))
+            flat = flatten_kd(obj)
+            got = DeviceKd(mesh, flat)
+            got.node_index = flat["_node_index"]
+            got.is_internal = flat["axis"] >= 0
         else:
             got = DeviceBvh(mesh, flatten_bvh(obj))
         _struct_cache[obj] = got
@@ -344,11 +403,17 @@ def bvh_intersect(bvh, ray: Ray) -> tuple[Optional[Hit], TraversalStats]:
 
 
 def kd_intersect(kd, ray: Ray, start_leaf=None) -> tuple[Optional[Hit], TraversalStats]:
-    """accel.py:761-832 on the device (start leaf by locate_leaf)."""
-    if start_leaf is not None:
-        raise NotImplementedError("explicit start_leaf is not supported; the device locates it")
+    """accel.py:761-832 on the device.  ``start_leaf``: a leaf node of ``kd``
+    (as the reference takes it) or its preorder index in the flattened tree;
+    None locates the origin's leaf (locate_leaf, accel.py:712-724)."""
     d = _device_struct(kd)
-    o = d.trace(_ray_array([ray]))
+    start = None
+    if start_leaf is not None:
+        k = start_leaf if isinstance(start_leaf, (int, np.integer)) else d.node_index.get(id(start_leaf))
+        if k is None or not (0 <= int(k) < d.num_nodes) or d.is_internal[int(k)]:
+            raise ValueError("start_leaf is not a leaf of this kd-tree")
+        start = np.array([int(k)], np.int32)
+    o = d.trace(_ray_array([ray]), start)
     if int(o["status"][0]) & (_lib.ST_ERROR | _lib.ST_OVERFLOW):
         raise TraversalError("kd walk did not terminate")
     stats = TraversalStats(kd_nodes_visited=int(o["nodes"][0]), kd_rope_steps=int(o["ropes"][0]),

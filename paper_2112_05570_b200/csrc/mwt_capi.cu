@@ -306,6 +306,16 @@ int mwt_raygen_dev(int mode, const double *box, uint64_t seed, uint64_t first, i
     return MWT_OK;
 }
 
+int mwt_locate_brute_dev(const mwt_mesh *m, const double *pts, int64_t n, int32_t *out_tid,
+                         uint32_t *out_status, void *stream) {
+    if (!m || n < 0 || (n > 0 && !pts)) return fail(MWT_E_INVALID, "locate_brute: bad argument");
+    if (m->dev.nt == 0) return fail(MWT_E_INVALID, "locate_brute: mesh has no triangles");
+    DeviceGuard g(m->device);
+    int rc = mwt::launch_locate(m->dev, pts, n, out_tid, out_status, stream, true);
+    if (rc) return cuda_fail((cudaError_t)rc, "locate_brute launch");
+    return MWT_OK;
+}
+
 int mwt_locate_dev(const mwt_mesh *m, const double *pts, int64_t n, int32_t *out_tid,
                    uint32_t *out_status, void *stream) {
     if (!m || n < 0 || (n > 0 && !pts)) return fail(MWT_E_INVALID, "locate: bad argument");
@@ -583,12 +593,13 @@ int mwt_kd_destroy(mwt_kd *k) {
     return MWT_OK;
 }
 
-int mwt_kd_trace_dev(const mwt_kd *k, const double *rays, int64_t n, int32_t *out_seg,
-                     double *out_t, double *out_u, int32_t *out_nodes, int32_t *out_rope_steps,
-                     int32_t *out_prim_tests, uint32_t *out_status, void *stream) {
+int mwt_kd_trace_dev(const mwt_kd *k, const double *rays, const int32_t *start_leaf, int64_t n,
+                     int32_t *out_seg, double *out_t, double *out_u, int32_t *out_nodes,
+                     int32_t *out_rope_steps, int32_t *out_prim_tests, uint32_t *out_status,
+                     void *stream) {
     if (!k || n < 0 || (n > 0 && !rays)) return fail(MWT_E_INVALID, "kd_trace: bad argument");
     DeviceGuard g(k->mesh->device);
-    int rc = mwt::launch_kd(k->mesh->dev, k->dev, rays, n, out_seg, out_t, out_u, out_nodes,
+    int rc = mwt::launch_kd(k->mesh->dev, k->dev, rays, start_leaf, n, out_seg, out_t, out_u, out_nodes,
                             out_rope_steps, out_prim_tests, out_status, stream);
     if (rc) return cuda_fail((cudaError_t)rc, "kd_trace launch");
     return MWT_OK;

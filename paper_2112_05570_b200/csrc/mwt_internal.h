@@ -180,7 +180,7 @@ struct KdDev {
 int launch_raygen(int mode, const double *box, uint64_t seed, uint64_t first, int64_t n,
                   double *rays, void *stream);
 int launch_locate(const MeshDev &m, const double *pts, int64_t n, int32_t *tid, uint32_t *st,
-                  void *stream);
+                  void *stream, bool brute = false);
 int launch_trace(const MeshDev &m, const double *rays, const int32_t *start, int64_t n,
                  int32_t *o_start, int32_t *o_seg, double *o_t, double *o_u, int32_t *o_steps,
                  uint32_t *o_st, void *stream, int32_t *o_end = nullptr);
@@ -196,7 +196,7 @@ int launch_histogram(const int32_t *seg, const int32_t *steps, const uint32_t *s
 int launch_bvh(const MeshDev &m, const BvhDev &b, const double *rays, int64_t n, int32_t *o_seg,
                double *o_t, double *o_u, int32_t *o_nodes, int32_t *o_prims, uint32_t *o_st,
                void *stream);
-int launch_kd(const MeshDev &m, const KdDev &k, const double *rays, int64_t n, int32_t *o_seg,
+int launch_kd(const MeshDev &m, const KdDev &k, const double *rays, const int32_t *start, int64_t n, int32_t *o_seg,
               double *o_t, double *o_u, int32_t *o_nodes, int32_t *o_ropes, int32_t *o_prims,
               uint32_t *o_st, void *stream);
 int launch_brute(const MeshDev &m, const double *rays, int64_t n, int32_t *o_seg, double *o_t,

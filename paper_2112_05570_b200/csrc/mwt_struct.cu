@@ -151,7 +151,7 @@ __device__ __forceinline__ int kd_descend(const KdDev &K, int node, double px, d
 }
 
 __global__ void __launch_bounds__(kThreads) k_kd(MeshDev M, KdDev K, const double *rays,
-                                                 long long n, int32_t *o_seg, double *o_t,
+                                                 const int32_t *start, long long n, int32_t *o_seg, double *o_t,
                                                  double *o_u, int32_t *o_nodes, int32_t *o_ropes,
                                                  int32_t *o_prims, uint32_t *o_st) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -164,8 +164,17 @@ __global__ void __launch_bounds__(kThreads) k_kd(MeshDev M, KdDev K, const doubl
         int tested[kKdMailbox];
         int ntested = 0;
         int dummy = 0;
-        int cur = kd_descend(K, 0, r.ox, r.oy, r.dx, r.dy, dummy, false);  // locate_leaf
+        int cur;
         long long guard = 4LL * K.nleaves + 16;
+        if (start) {  // kd_intersect(kd, ray, start_leaf): the given leaf (accel.py:771)
+            cur = __ldg(start + i);
+            if (cur < 0 || cur >= K.nnodes || __ldg(K.axis + cur) >= 0) {
+                cur = 0;
+                guard = 0;  // not a leaf: reported as an error
+            }
+        } else {
+            cur = kd_descend(K, 0, r.ox, r.oy, r.dx, r.dy, dummy, false);  // locate_leaf
+        }
         while (guard > 0 && !done) {
             guard--;
             nodes++;
@@ -318,11 +327,11 @@ int launch_bvh(const MeshDev &m, const BvhDev &b, const double *rays, int64_t n,
     MWT_LAUNCH_RET;
 }
 
-int launch_kd(const MeshDev &m, const KdDev &k, const double *rays, int64_t n, int32_t *o_seg,
+int launch_kd(const MeshDev &m, const KdDev &k, const double *rays, const int32_t *start, int64_t n, int32_t *o_seg,
               double *o_t, double *o_u, int32_t *o_nodes, int32_t *o_ropes, int32_t *o_prims,
               uint32_t *o_st, void *stream) {
     if (n <= 0) return 0;
-    k_kd<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(m, k, rays, n, o_seg, o_t, o_u,
+    k_kd<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(m, k, rays, start, n, o_seg, o_t, o_u,
                                                              o_nodes, o_ropes, o_prims, o_st);
     MWT_LAUNCH_RET;
 }

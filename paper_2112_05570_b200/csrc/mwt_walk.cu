@@ -983,6 +983,11 @@ __global__ void __launch_bounds__(kThreads) k_raygen(const __grid_constant__ Ray
     }
 }
 
+// BRUTE: locate_triangle(tri, p, "brute") (accel.py:341-349): the first
+// triangle in id order that _contains p -- the lowest containing id, so the
+// tie flood from it returns it unchanged -- else the nearest centroid
+// (accel.py:241-253; no neighbour of it contains p either)
+template <bool BRUTE>
 __global__ void __launch_bounds__(kThreads) k_locate(MeshDev M, const double *pts, long long n,
                                                      int32_t *tid, uint32_t *st) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
@@ -990,7 +995,14 @@ __global__ void __launch_bounds__(kThreads) k_locate(MeshDev M, const double *pt
         double2 p = __ldg(reinterpret_cast<const double2 *>(pts) + i);
         uint32_t s = 0;
         double2 P0, P1, P2;
-        int t = locate(M, p.x, p.y, s, P0, P1, P2);
+        int t;
+        if (BRUTE) {
+            const LocRes lr = loc_brute(M.cxy, M.nt, p.x, p.y);
+            t = lr.tid;
+            s = ST_LOC_BRUTE | lr.st;
+        } else {
+            t = locate(M, p.x, p.y, s, P0, P1, P2);
+        }
         if (tid) tid[i] = t;
         if (st) st[i] = s;
     }
@@ -1122,9 +1134,12 @@ int launch_raygen(int mode, const double *box, uint64_t seed, uint64_t first, in
 }
 
 int launch_locate(const MeshDev &m, const double *pts, int64_t n, int32_t *tid, uint32_t *st,
-                  void *stream) {
+                  void *stream, bool brute) {
     if (n <= 0) return 0;
-    k_locate<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(m, pts, n, tid, st);
+    if (brute)
+        k_locate<true><<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(m, pts, n, tid, st);
+    else
+        k_locate<false><<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(m, pts, n, tid, st);
     MWT_LAUNCH_RET;
 }
 

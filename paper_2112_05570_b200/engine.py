@@ -210,11 +210,22 @@ class DeviceMesh:
     def _to_dev(self, a: np.ndarray) -> torch.Tensor:
         return torch.from_numpy(np.ascontiguousarray(a)).to(self._dev())
 
-    def locate(self, pts: np.ndarray):
+    def locate_brute_device(self, pts: torch.Tensor, stream=None):
+        """locate_triangle(tri, p, "brute"): lowest containing id, else nearest centroid."""
+        pts = _held(pts, stream)
+        n = pts.shape[0]
+        tid = torch.empty(n, dtype=torch.int32, device=pts.device)
+        st = torch.empty(n, dtype=torch.int32, device=pts.device)
+        check(lib.mwt_locate_brute_dev(self._h, ptr(pts), n, ptr(tid), ptr(st), _stream(stream, self.device)),
+              "locate_brute")
+        return tid, st
+
+    def locate(self, pts: np.ndarray, method: str = "anchor"):
         pts = _f64(pts).reshape(-1, 2)
         if len(pts) == 0:
             return np.zeros(0, np.int32), np.zeros(0, np.uint32)
-        tid, st = self.locate_device(self._to_dev(pts))
+        fn = self.locate_brute_device if method == "brute" else self.locate_device
+        tid, st = fn(self._to_dev(pts))
         torch.cuda.synchronize(self.device)
         return tid.cpu().numpy(), st.cpu().numpy().view(np.uint32)
 
@@ -322,8 +333,10 @@ class DeviceKd:
         except Exception:
             pass
 
-    def trace_device(self, rays: torch.Tensor, stream=None) -> dict:
-        rays = _held(rays, stream)
+    def trace_device(self, rays: torch.Tensor, start_leaf: torch.Tensor | None = None, stream=None) -> dict:
+        """``start_leaf``: per-ray node indices of the leaves to start from
+        (kd_intersect's start_leaf), else each ray's origin leaf."""
+        rays, start_leaf = _held(rays, stream), _held(start_leaf, stream)
         n = rays.shape[0]
         d = rays.device
         out = dict(seg=torch.empty(n, dtype=torch.int32, device=d),
@@ -333,14 +346,16 @@ class DeviceKd:
                    ropes=torch.empty(n, dtype=torch.int32, device=d),
                    prims=torch.empty(n, dtype=torch.int32, device=d),
                    status=torch.empty(n, dtype=torch.int32, device=d))
-        check(lib.mwt_kd_trace_dev(self._h, ptr(rays), n, ptr(out["seg"]), ptr(out["t"]),
+        check(lib.mwt_kd_trace_dev(self._h, ptr(rays), ptr(start_leaf), n, ptr(out["seg"]), ptr(out["t"]),
                                    ptr(out["u"]), ptr(out["nodes"]), ptr(out["ropes"]),
                                    ptr(out["prims"]), ptr(out["status"]), _stream(stream, self.mesh.device)), "kd_trace")
         return out
 
-    def trace(self, rays: np.ndarray) -> dict:
+    def trace(self, rays: np.ndarray, start_leaf: np.ndarray | None = None) -> dict:
         rays = _f64(rays).reshape(-1, 4)
-        out = self.trace_device(torch.from_numpy(rays).to(self.mesh._dev()))
+        dev = self.mesh._dev()
+        s = None if start_leaf is None else torch.from_numpy(_i32(start_leaf)).to(dev)
+        out = self.trace_device(torch.from_numpy(rays).to(dev), s)
         torch.cuda.synchronize(self.mesh.device)
         return {k: v.cpu().numpy() for k, v in out.items()}
 

@@ -9,6 +9,7 @@ returns.  Outputs (committed): tests/golden/*.npz.
   struct_<c>.npz  per config: reference bvh/kd results + counters on a ray subset
   hypot.npz     math.hypot values (CPython's is correctly rounded)
   degenerate.npz  rays where the reference walk and brute force disagree
+  kdstart.npz   kd_intersect from given start leaves (accel.py:761-771)
   branches.npz  hand-built inputs forcing the walk's fallback / TraversalError /
                 parallel-exit branches and outside-the-mesh locates
 
@@ -504,6 +505,38 @@ def make_branches():
     np.savez_compressed(os.path.join(HERE, "branches.npz"), **out)
 
 
+def make_kdstart(nrays=2000):
+    """kd_intersect(kd, ray, start_leaf=leaf) (accel.py:761-771) from random
+    leaves of the reference-built Lines-1024 kd-tree (c_t = 1): results,
+    counters and errors, with each leaf's preorder index in the flattened tree."""
+    from paper_2112_05570_b200.accel import flatten_kd
+    d = os.path.join(FIX, "lines1024")
+    scene = Scene.load(os.path.join(d, "scene.txt"))
+    kd = build_kdtree(scene, 1.0)
+    flat = flatten_kd(kd)
+    index = flat.pop("_node_index")
+    rng = np.random.default_rng(17)
+    arr = raygen(1, (0.0, 0.0, 1.0, 1.0), 55, 0, nrays)
+    leaves = rng.integers(0, len(kd._leaves), nrays)
+    out = {k: v for k, v in flat.items()}
+    out["rays"] = arr
+    out["start"] = np.array([index[id(kd._leaves[k])] for k in leaves], np.int32)
+    seg, t, nodes, ropes, prims, err = [], [], [], [], [], []
+    for r, k in zip(rays_from(arr), leaves):
+        try:
+            h, st = kd_intersect(kd, r, start_leaf=kd._leaves[k])
+        except TraversalError:
+            seg.append(-1); t.append(np.nan); nodes.append(-1); ropes.append(-1); prims.append(-1); err.append(1)
+            continue
+        seg.append(-1 if h is None else h.seg); t.append(np.nan if h is None else h.t)
+        nodes.append(st.kd_nodes_visited); ropes.append(st.kd_rope_steps); prims.append(st.kd_prim_tests)
+        err.append(0)
+    out.update(seg=np.array(seg, np.int32), t=np.array(t), nodes=np.array(nodes, np.int32),
+               ropes=np.array(ropes, np.int32), prims=np.array(prims, np.int32), error=np.array(err, np.uint8))
+    print(f"kdstart: {nrays} rays, {int(np.sum(err))} errors, hits {int((out['seg'] >= 0).sum())}", flush=True)
+    np.savez_compressed(os.path.join(HERE, "kdstart.npz"), **out)
+
+
 if __name__ == "__main__":
     groups = sys.argv[1:] or ["known", "hypot"] + [f"config:{c}" for c in CONFIGS] + \
         [f"struct:{c}" for c in CONFIGS[1:]]
@@ -518,6 +551,8 @@ if __name__ == "__main__":
             make_degenerate()
         elif g == "branches":
             make_branches()
+        elif g == "kdstart":
+            make_kdstart()
         elif g.startswith("config:"):
             make_config(g.split(":", 1)[1])
         elif g.startswith("struct:"):

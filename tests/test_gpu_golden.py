@@ -133,3 +133,130 @@ def test_degenerate_rays_on_device():
             assert int(bf["seg"][0]) == int(g[f"{k}_brute"][0]) and bf["t"][0] == g[f"{k}_brute"][1]
         k += 1
     assert k > 0
+
+
+def _branch_cases():
+    p = os.path.join(GOLDEN, "branches.npz")
+    return [str(c) for c in np.load(p)["cases"]] if os.path.exists(p) else []
+
+
+LOCATED = ("parallel_exit", "outside_")  # starts located by the reference's TriLocator
+
+
+@pytest.mark.parametrize("name", _branch_cases())
+def test_branch_fixtures_on_device(name):
+    """The walk's fallback exit, both TraversalError kinds, the parallel branch
+    at a constrained exit and outside-the-mesh locates (tests/golden/branches.npz,
+    recorded from the reference): the device reproduces the reference's
+    outcomes and sets exactly the oracle's status bits."""
+    from oracle import oracle as orc
+    from paper_2112_05570_b200 import _lib
+    g = _golden("branches.npz")
+    m = _mesh(g, name)
+    rays = g[f"{name}__rays"]
+    given = None if name.startswith(LOCATED) else g[f"{name}__w_start"]
+    out = m.trace(rays, given)
+    _check(out, g, f"{name}__w_")
+    # status bits: the oracle's, bit for bit (minus the engine's own seed-search notes)
+    sc = orc.RawScene(*(np.ascontiguousarray(g[f"{name}__seg_xy"][:, k]) for k in range(4)),
+                      np.ascontiguousarray(g[f"{name}__seg_kind"]))
+    vxy = g[f"{name}__vxy"]
+    om = orc.Mesh(sc, orc.RawTri(np.ascontiguousarray(vxy[:, 0]), np.ascontiguousarray(vxy[:, 1]),
+                                 np.ascontiguousarray(g[f"{name}__v"]), np.ascontiguousarray(g[f"{name}__nbr"]),
+                                 np.ascontiguousarray(g[f"{name}__flag"])))
+    ref = om.trace(rays, given)
+    mask = np.uint32(~_lib.ST_ENGINE_ONLY & 0xFFFFFFFF)
+    assert np.array_equal(out["status"].view(np.uint32) & mask, ref["status"] & mask)
+    if f"{name}__loc_pts" in g.files:
+        pts = g[f"{name}__loc_pts"]
+        tid, st = m.locate(pts)
+        assert np.array_equal(tid, g[f"{name}__loc_anchor"])
+        assert (st & _lib.ST_LOC_OUTSIDE).all()
+        tb, _ = m.locate(pts, method="brute")
+        assert np.array_equal(tb, g[f"{name}__loc_brute"])
+
+
+def test_branch_fixtures_through_the_drop_in():
+    """The drop-in raises TraversalError on exactly the rays where the reference
+    raised it (revisit and no-exit kinds), and returns its hits elsewhere."""
+    from paper_2112_05570_b200 import accel
+    from paper_2112_05570_b200.formats import SceneArrays, TriArrays
+    from paper_2112_05570_b200.geometry import Point, Ray
+    from paper_2112_05570_b200.model import Scene, Triangulation
+    g = _golden("branches.npz")
+    raised = {1: 0, 2: 0}
+    for name in _branch_cases():
+        if not name.startswith("fan"):
+            continue
+        scene = Scene.from_arrays(SceneArrays(g[f"{name}__seg_xy"], g[f"{name}__seg_kind"]))
+        tri = Triangulation.from_arrays(scene, TriArrays(g[f"{name}__vxy"], g[f"{name}__v"], g[f"{name}__nbr"],
+                                                          g[f"{name}__flag"]))
+        rays, err = g[f"{name}__rays"], g[f"{name}__w_error"]
+        sel = np.concatenate([np.nonzero(err)[0], np.nonzero(err == 0)[0][:40]])
+        for i in sel:
+            r = rays[i]
+            ray = Ray(Point(r[0], r[1]), Point(r[2], r[3]))
+            start = int(g[f"{name}__w_start"][i])
+            if err[i]:
+                with pytest.raises(accel.TraversalError):
+                    accel.traverse_triangulation(tri, ray, start)
+                raised[int(err[i])] += 1
+            else:
+                hit, stats = accel.traverse_triangulation(tri, ray, start)
+                assert stats.tri_steps == g[f"{name}__w_steps"][i]
+                assert (hit is None) == (g[f"{name}__w_seg"][i] < 0)
+                if hit is not None:
+                    assert hit.seg == g[f"{name}__w_seg"][i] and hit.t == g[f"{name}__w_t"][i]
+    assert raised[1] > 0 and raised[2] > 0
+
+
+def test_drop_in_repacks_an_edited_triangulation():
+    """the reference edits triangulations in place; the drop-in's
+    cached device copy must follow (content fingerprint), not walk a stale mesh."""
+    from paper_2112_05570_b200 import accel
+    from paper_2112_05570_b200.geometry import Point, Ray
+    from paper_2112_05570_b200.model import Scene, load_triangulation
+    paths = fixture_paths("lines64", "mwt")
+    scene = Scene.load(paths[0])
+    tri = load_triangulation(paths[1], scene)
+    ray = Ray(Point(0.0, 0.37), Point(1.0, 0.0))
+    loc = accel.TriLocator(tri)
+    s0 = loc.locate(ray.origin)
+    h0, st0 = accel.traverse_triangulation(tri, ray, s0)
+    # move every vertex by a tiny shear: the same topology, different geometry
+    for v in tri.verts:
+        v.x, v.y = v.x, v.y + 1e-3 * v.x
+    s1 = loc.locate(ray.origin)
+    h1, st1 = accel.traverse_triangulation(tri, ray, s1)
+    from oracle import oracle as orc
+    from paper_2112_05570_b200.accel import _TriMap
+    arr = _TriMap(tri).arrays
+    om = orc.Mesh(orc.RawScene(*(np.ascontiguousarray(scene.to_arrays().xy[:, k]) for k in range(4)),
+                               np.ascontiguousarray(scene.to_arrays().kind)),
+                  orc.RawTri(np.ascontiguousarray(arr.vxy[:, 0]), np.ascontiguousarray(arr.vxy[:, 1]),
+                             np.ascontiguousarray(arr.v), np.ascontiguousarray(arr.nbr),
+                             np.ascontiguousarray(arr.flag)))
+    ref = om.trace(np.array([[0.0, 0.37, 1.0, 0.0]]))
+    assert s1 == ref["start"][0] and st1.tri_steps == ref["steps"][0]
+    assert (h1 is None and ref["seg"][0] < 0) or (h1.seg == ref["seg"][0] and h1.t == ref["t"][0])
+    assert (st1.tri_steps, getattr(h1, "t", None)) != (st0.tri_steps, getattr(h0, "t", None))
+
+
+def test_kd_from_given_start_leaves():
+    """kd_intersect(kd, ray, start_leaf=...) (accel.py:761-771) from random
+    leaves: hit and all three counters equal the reference's (kdstart.npz);
+    a start index that is not a leaf is an error, and the drop-in rejects it."""
+    from paper_2112_05570_b200 import _lib, accel
+    from paper_2112_05570_b200.engine import DeviceKd, DeviceMesh
+    g = _golden("kdstart.npz")
+    mesh = DeviceMesh.from_files(*fixture_paths("lines1024", "mwt"))
+    kd = DeviceKd(mesh, {k: g[k] for k in g.files})
+    o = kd.trace(g["rays"], g["start"])
+    assert not (o["status"] & _lib.ST_ERROR).any() and not g["error"].any()
+    for k in ("seg", "nodes", "ropes", "prims"):
+        assert np.array_equal(o[k], g[k]), k
+    hit = g["seg"] >= 0
+    assert np.array_equal(o["t"][hit], g["t"][hit])
+    internal = int(np.nonzero(g["axis"] >= 0)[0][0])
+    bad = kd.trace(g["rays"][:2], np.array([internal, -1], np.int32))
+    assert (bad["status"] & _lib.ST_ERROR).all()
