@@ -203,17 +203,45 @@ __device__ __forceinline__ unsigned long long draw(const RayGen &g, unsigned lon
     return (z & ~g.cmask) | (mix64(gs + (unsigned long long)(k + 1) * kGolden) & g.cmask);
 }
 
-// rejection attempt a: one 64-bit draw -> two 32-bit coordinates in [-1, 1)
-__device__ __forceinline__ void disk_try(const RayGen &g, unsigned long long s0, unsigned long long gs,
-                                         int a, double &x, double &y, double &r2) {
-    const unsigned long long z = draw(g, s0, gs, (unsigned)a);
-    // x = 2 * (hi * 2^-32) - 1, built without an integer conversion: the double
-    // 2 + hi * 2^-31 has hi in its top mantissa bits, and subtracting 3 is exact
-    // (both forms are exact, so the bits agree with the host twins)
+// 64-bit draw -> two 32-bit coordinates in [-1, 1): x = 2 * (hi * 2^-32) - 1,
+// built without an integer conversion: the double 2 + hi * 2^-31 has hi in its
+// top mantissa bits, and subtracting 3 is exact (both forms are exact, so the
+// bits agree with the host twins)
+__device__ __forceinline__ void disk_point(unsigned long long z, double &x, double &y, double &r2) {
     const unsigned hi = (unsigned)(z >> 32), lo = (unsigned)z;
     x = __hiloint2double((int)(0x40000000u | (hi >> 12)), (int)(hi << 20)) - 3.0;
     y = __hiloint2double((int)(0x40000000u | (lo >> 12)), (int)(lo << 20)) - 3.0;
     r2 = x * x + y * y;
+}
+
+// rejection attempt a: one 64-bit draw -> two 32-bit coordinates in [-1, 1)
+__device__ __forceinline__ void disk_try(const RayGen &g, unsigned long long s0, unsigned long long gs,
+                                         int a, double &x, double &y, double &r2) {
+    disk_point(draw(g, s0, gs, (unsigned)a), x, y, r2);
+}
+
+// Group words of draws 0 and 128 for the calling lanes (coherent order).  The
+// lanes of one refill batch take consecutive ray indices, so nearly always
+// they share one group: the first two active lanes compute its two words
+// (one mix64 pass for the warp instead of two) and broadcast them; lanes of
+// another group (a batch across a group boundary) compute their own.
+__device__ __forceinline__ void group_words(unsigned long long gs, unsigned long long &w0,
+                                            unsigned long long &w128) {
+    const unsigned m = __activemask();
+    const int lane = threadIdx.x & 31;
+    const int l0 = __ffs(m) - 1;
+    const unsigned m1 = m & (m - 1u);
+    const int l1 = m1 ? __ffs(m1) - 1 : l0;
+    const unsigned long long gl = __shfl_sync(m, gs, l0);
+    // lane l1 computes draw 128 of the leader's group, every other lane draw 0
+    const unsigned long long v = mix64(gl + ((lane == l1 && l1 != l0) ? 129ull : 1ull) * kGolden);
+    w0 = __shfl_sync(m, v, l0);
+    w128 = __shfl_sync(m, v, l1);
+    if (l1 == l0) w128 = mix64(gl + 129ull * kGolden);  // a single active lane
+    if (gs != gl) {  // (rare) a lane of another group
+        w0 = mix64(gs + kGolden);
+        w128 = mix64(gs + 129ull * kGolden);
+    }
 }
 
 __device__ __forceinline__ Ray gen_ray(const RayGen &g, unsigned long long idx) {
@@ -221,22 +249,24 @@ __device__ __forceinline__ Ray gen_ray(const RayGen &g, unsigned long long idx) 
     const unsigned long long s0 = g.key ^ idx;
     const unsigned long long gs = g.gkey ^ (idx >> g.gshift);  // the group's stream
     const Box &b = g.box;
-    // unit-disk rejection: the first accepted attempt a in 0..63.  Attempts 0
-    // and 1 are evaluated unconditionally (accepted together with probability
-    // 1 - (1 - pi/4)^2 = 95%) so the warp stays converged; the rest is a rare loop.
-    double xa, ya, ra, xb, yb, rb;
-    disk_try(g, s0, gs, 0, xa, ya, ra);
-    disk_try(g, s0, gs, 1, xb, yb, rb);
-    const bool oka = ra <= 1.0 && ra > 0x1p-60, okb = rb <= 1.0 && rb > 0x1p-60;
-    double x = oka ? xa : xb, y = oka ? ya : yb, r2 = oka ? ra : rb;
-    bool ok = oka || okb;
-    if (!ok) {
-        for (int a = 2; a < 64; a++) {
-            disk_try(g, s0, gs, a, x, y, r2);
-            if (r2 <= 1.0 && r2 > 0x1p-60) {
-                ok = true;
-                break;
-            }
+    const unsigned m = __activemask();
+    unsigned long long G0 = 0ull, G128 = 0ull;
+    if (g.cmask) group_words(gs, G0, G128);
+    // unit-disk rejection: the first accepted attempt a in 0..63.  Later
+    // attempts run while any lane of the warp still needs one (iid order:
+    // nearly every warp needs attempt 1; coherent order: only a group whose
+    // attempt-0 cell lies outside the disk), so the warp stays converged.
+    double x, y, r2;
+    disk_point((mix64(s0 + kGolden) & ~g.cmask) | (G0 & g.cmask), x, y, r2);
+    bool ok = r2 <= 1.0 && r2 > 0x1p-60;
+    for (int a = 1; a < 64 && __any_sync(m, !ok); a++) {
+        if (!ok) {
+            double xa, ya, ra;
+            disk_try(g, s0, gs, a, xa, ya, ra);
+            ok = ra <= 1.0 && ra > 0x1p-60;
+            x = xa;
+            y = ya;
+            r2 = ra;
         }
     }
     Ray r;
@@ -251,7 +281,7 @@ __device__ __forceinline__ Ray gen_ray(const RayGen &g, unsigned long long idx) 
     const double W = b.x1 - b.x0, H = b.y1 - b.y0;
     // u, v: the two 32-bit halves of draw 128 (hi * 2^-32, lo * 2^-32), built
     // as 1 + h * 2^-32 - 1 (exact)
-    const unsigned long long zuv = draw(g, s0, gs, 128u);
+    const unsigned long long zuv = (mix64(s0 + 129ull * kGolden) & ~g.cmask) | (G128 & g.cmask);
     const unsigned uh = (unsigned)(zuv >> 32), vl = (unsigned)zuv;
     const double u = __hiloint2double((int)(0x3FF00000u | (uh >> 12)), (int)(uh << 20)) - 1.0;
     const double v = __hiloint2double((int)(0x3FF00000u | (vl >> 12)), (int)(vl << 20)) - 1.0;

@@ -27,7 +27,6 @@ the final file is tests/golden/digests_<mesh>.json.
 from __future__ import annotations
 
 import argparse
-import hashlib
 import json
 import multiprocessing as mp
 import os
@@ -50,20 +49,8 @@ PARTS = {
     "hair512": ((0.0, 0.0, 1.0, 1.0), [(0, 1 << 24)]),
     "floorplan64": ((0.0, 0.0, 1.0, 1.0), [(0, 1 << 26)]),
 }
-NAN = np.frombuffer(np.uint64(0x7FF8000000000000).tobytes(), np.float64)[0]
-
-
-def digest_walk(seg, t, steps) -> str:
-    t = np.where(np.isnan(t), NAN, t).astype(np.float64)
-    h = hashlib.sha256()
-    h.update(np.ascontiguousarray(seg, np.int32).tobytes())
-    h.update(np.ascontiguousarray(t).tobytes())
-    h.update(np.ascontiguousarray(steps, np.int32).tobytes())
-    return h.hexdigest()
-
-
-def digest_start(start) -> str:
-    return hashlib.sha256(np.ascontiguousarray(start, np.int32).tobytes()).hexdigest()
+sys.path.insert(0, os.path.dirname(HERE))
+from digests import digest_start, digest_walk  # noqa: E402  (tests/digests.py, shared with the tests)
 
 
 _W = {}

@@ -302,3 +302,29 @@ def test_branch_fixtures_reach_every_branch():
     for b in (orc.ST_ERROR, orc.ST_FALLBACK, orc.ST_PARALLEL, orc.ST_GRAZING, orc.ST_ZERO_SIDE,
               orc.ST_LOC_OUTSIDE, orc.ST_LOC_BRUTE, orc.ST_MULTI, orc.ST_LOC_TIE):
         assert bits & b, f"status bit {b} never set"
+
+
+@pytest.mark.parametrize("mesh", ["mwt", "cdt"])
+def test_oracle_matches_full_set_reference_digests_on_sample_chunks(mesh):
+    """The reference's per-chunk digests over the full BASELINE ray sets
+    (tests/golden/make_digests.py): the oracle reproduces the first, a middle
+    and the last chunk of every config's parts on CPU (the GPU test covers every
+    chunk on the device and with the oracle)."""
+    import digests as dg
+    D = dg.load(mesh)
+    if D is None or not D["configs"]:
+        pytest.skip(f"reference digests for {mesh} not recorded")
+    chunk = D["chunk"]
+    for cfg, C in D["configs"].items():
+        m = orc.Mesh.from_files(*fixture_paths(cfg, mesh))
+        for part in C["parts"]:
+            base, n, ref_chunks = part["mode"], part["n"], part["chunks"]
+            mode = rg.coherent(base)
+            nc = len(ref_chunks)
+            for c in sorted({0, nc // 2, nc - 1}):
+                lo = c * chunk
+                k = min(chunk, n - lo)
+                out = m.trace(orc.raygen(mode, tuple(C["box"]), D["seed"], lo, k))
+                err = (out["status"] & orc.ST_ERROR) != 0
+                (dw, ds), = dg.chunk_digests(out["seg"], out["t"], out["steps"], out["start"], err, chunk)
+                assert (dw, ds) == tuple(ref_chunks[c][:2]), f"{cfg} part {base} chunk {c}"
