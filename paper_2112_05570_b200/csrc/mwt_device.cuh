@@ -253,13 +253,24 @@ __device__ __forceinline__ Ray gen_ray(const RayGen &g, unsigned long long idx) 
     unsigned long long G0 = 0ull, G128 = 0ull;
     if (g.cmask) group_words(gs, G0, G128);
     // unit-disk rejection: the first accepted attempt a in 0..63.  Later
-    // attempts run while any lane of the warp still needs one (iid order:
-    // nearly every warp needs attempt 1; coherent order: only a group whose
-    // attempt-0 cell lies outside the disk), so the warp stays converged.
+    // attempts run while any lane of the warp still needs one, so the warp
+    // stays converged (iid order: attempt 1 always -- nearly every warp needs
+    // it; coherent order: only a group whose attempt-0 cell missed the disk).
     double x, y, r2;
     disk_point((mix64(s0 + kGolden) & ~g.cmask) | (G0 & g.cmask), x, y, r2);
     bool ok = r2 <= 1.0 && r2 > 0x1p-60;
-    for (int a = 1; a < 64 && __any_sync(m, !ok); a++) {
+    int a0 = 1;
+    if (!g.cmask) {
+        // iid order: attempt 1 unconditionally (nearly every warp needs it)
+        double xb, yb, rb;
+        disk_point(mix64(s0 + 2ull * kGolden), xb, yb, rb);
+        x = ok ? x : xb;
+        y = ok ? y : yb;
+        r2 = ok ? r2 : rb;
+        ok = ok || (rb <= 1.0 && rb > 0x1p-60);
+        a0 = 2;
+    }
+    for (int a = a0; a < 64 && __any_sync(m, !ok); a++) {
         if (!ok) {
             double xa, ya, ra;
             disk_try(g, s0, gs, a, xa, ya, ra);

@@ -670,6 +670,39 @@ __device__ __forceinline__ void epilogue(const MeshDev *__restrict__ Mg, const L
 }
 
 
+// The step record k of the tight loop: the two candidate exit words (E1 =
+// edge (j+1)%3, E2 = edge (j+2)%3) and the apex corner -- from the staged
+// per-record table (SMEM), the staged per-triangle table (SMEM && TRI) or one
+// 32-B global record.
+template <bool SMEM, bool TRI>
+__device__ __forceinline__ void fetch_step(const MeshDev &M, const uint2 *srec, const uint4 *stri,
+                                           const double2 *svxy, uint32_t k, uint32_t &wx, uint32_t &wy,
+                                           double2 &A) {
+    if (SMEM && TRI) {
+        // record 3N + j from triangle N's 16-B entry: apex = corner j,
+        // exits = edges (j+1)%3, (j+2)%3
+        const uint32_t N = __umulhi(k, 0xAAAAAAABu) >> 1;
+        const uint32_t j = k - 3u * N;
+        const uint4 X = stri[N];
+        const uint32_t a = j == 0u ? X.x : (j == 1u ? X.y : X.z);
+        const uint32_t b = j == 0u ? X.y : (j == 1u ? X.z : X.x);
+        const uint32_t c = j == 0u ? X.z : (j == 1u ? X.x : X.y);
+        A = svxy[a >> kCVidShift];
+        wx = b & kCWordMask;
+        wy = c & kCWordMask;
+    } else if (SMEM) {
+        const uint2 X = srec[k];
+        A = svxy[X.x >> kCVidShift];
+        wx = X.x & kCWordMask;
+        wy = X.y;
+    } else {
+        int4 W;
+        load_step_issue(M, k, W, A);
+        wx = (uint32_t)W.x;
+        wy = (uint32_t)W.y;
+    }
+}
+
 #ifndef MWT_GRAB
 #define MWT_GRAB 128
 #endif
@@ -876,54 +909,54 @@ __global__ void __launch_bounds__(THREADS, MINB)
         // edge ends the lane's walk in the loop but its phase is set after it.
         const int glim = lim - kUnroll;
         bool fl = phase == 1 && s.fast && s.steps < glim;
+        const bool entered = fl;
+        // kn: the record of the triangle the lane enters next.  It stays a
+        // valid record index throughout the loop (a lane that left keeps
+        // re-reading its last record and commits nothing), so the load needs
+        // no select, and only kn and the step count change per step; the exit
+        // word, edge and triangle are recovered after the loop from record kn.
+        uint32_t kn = fl ? s.w : 0u;
         {
             const int thr = more ? refill_below : 0;
             while (__popc(__ballot_sync(FULL, fl)) > thr) {
 #pragma unroll
                 for (int u2 = 0; u2 < kUnroll; u2++) {
-                    // predicated, not branched: lanes that left compute on record 0
-                    // and commit nothing
-                    const uint32_t k = fl ? s.w : 0u;
                     uint32_t wx, wy;
                     double2 A;
-                    if (SMEM && TRI) {
-                        // record 3N + j from triangle N's 16-B entry: apex = corner j,
-                        // exits = edges (j+1)%3, (j+2)%3
-                        const uint32_t N = __umulhi(k, 0xAAAAAAABu) >> 1;
-                        const uint32_t j = k - 3u * N;
-                        const uint4 X = stri[N];
-                        const uint32_t a = j == 0u ? X.x : (j == 1u ? X.y : X.z);
-                        const uint32_t b = j == 0u ? X.y : (j == 1u ? X.z : X.x);
-                        const uint32_t c = j == 0u ? X.z : (j == 1u ? X.x : X.y);
-                        A = svxy[a >> kCVidShift];
-                        wx = b & kCWordMask;
-                        wy = c & kCWordMask;
-                    } else if (SMEM) {
-                        const uint2 X = srec[k];
-                        A = svxy[X.x >> kCVidShift];
-                        wx = X.x & kCWordMask;
-                        wy = X.y;
-                    } else {
-                        int4 W;
-                        load_step_issue(M, k, W, A);
-                        wx = (uint32_t)W.x;
-                        wy = (uint32_t)W.y;
-                    }
+                    fetch_step<SMEM, TRI>(M, srec, stri, svxy, kn, wx, wy, A);
                     const double c = side_of(r, A);
-                    const bool ok = fl && c != 0.0, pos = c > 0.0;
-                    const uint32_t nw = pos ? wx : wy;
+                    const bool ok = fl && c != 0.0;
+                    const uint32_t nw = c > 0.0 ? wx : wy;  // E1 if c > 0, else E2
                     s.steps += ok ? 1 : 0;
-                    s.kr = ok ? (int)k : s.kr;
-                    s.ch = ok ? (pos ? 0 : 1) : s.ch;
-                    s.w = ok ? nw : s.w;
-                    fl = ok && !(nw & (SMEM ? kCStop : kStopBit));
+                    const bool go = ok && !(nw & (SMEM ? kCStop : kStopBit));
+                    kn = go ? nw : kn;
+                    fl = go;
                 }
                 fl = fl && s.steps < glim;
             }
         }
-        // a phase-1 lane holds a stop word only if the loop just reached it
-        if (phase == 1 && (s.w & (SMEM ? (kStopBit | kCStop) : kStopBit))) phase = 2;
-        if (SMEM && (s.w & (kStopBit | kCStop)) == kCStop) s.w = expand_cword(s.w);
+        if (entered) {
+            if (fl || s.steps >= glim) {
+                s.w = kn;  // left behind in the fast state, or at the guard (walk_step flags it)
+            } else {
+                // the lane reached its stop edge in record kn, or met a zero
+                // apex side there (not counted; the general rule decides it):
+                // both are pure functions of the record and the ray
+                uint32_t wx, wy;
+                double2 A;
+                fetch_step<SMEM, TRI>(M, srec, stri, svxy, kn, wx, wy, A);
+                const double c = side_of(r, A);
+                if (c == 0.0) {
+                    s.w = kn;
+                } else {
+                    const uint32_t nw = c > 0.0 ? wx : wy;
+                    s.w = SMEM ? expand_cword(nw) : nw;
+                    s.kr = (int)kn;
+                    s.ch = c > 0.0 ? 0 : 1;
+                    phase = 2;
+                }
+            }
+        }
         // one full-rule step for every lane that left the tight loop still
         // walking (zero side, the general state, the guard); lanes it merely
         // left behind (still in the fast state) continue after the refill

@@ -213,33 +213,35 @@ def test_branch_fixtures_through_the_drop_in():
 def test_drop_in_repacks_an_edited_triangulation():
     """the reference edits triangulations in place; the drop-in's
     cached device copy must follow (content fingerprint), not walk a stale mesh."""
+    from oracle import oracle as orc
     from paper_2112_05570_b200 import accel
-    from paper_2112_05570_b200.geometry import Point, Ray
+    from paper_2112_05570_b200.accel import _TriMap
     from paper_2112_05570_b200.model import Scene, load_triangulation
     paths = fixture_paths("lines64", "mwt")
     scene = Scene.load(paths[0])
     tri = load_triangulation(paths[1], scene)
-    ray = Ray(Point(0.0, 0.37), Point(1.0, 0.0))
-    loc = accel.TriLocator(tri)
-    s0 = loc.locate(ray.origin)
-    h0, st0 = accel.traverse_triangulation(tri, ray, s0)
-    # move every vertex by a tiny shear: the same topology, different geometry
+    rays = orc.raygen(1, (0, 0, 1, 1), 3, 0, 4000)
+    p0 = accel.pack(tri)
+    before = accel.trace_batch(tri, rays)
+    # an in-place edit: shear every interior vertex (same topology, new geometry)
     for v in tri.verts:
-        v.x, v.y = v.x, v.y + 1e-3 * v.x
-    s1 = loc.locate(ray.origin)
-    h1, st1 = accel.traverse_triangulation(tri, ray, s1)
-    from oracle import oracle as orc
-    from paper_2112_05570_b200.accel import _TriMap
+        if 0.0 < v.x < 1.0 and 0.0 < v.y < 1.0:
+            v.x, v.y = v.x, v.y + 2e-3 * (v.x - 0.5)
+    p1 = accel.pack(tri)
+    assert p1 is not p0
+    after = accel.trace_batch(tri, rays)
+    sa = scene.to_arrays()
     arr = _TriMap(tri).arrays
-    om = orc.Mesh(orc.RawScene(*(np.ascontiguousarray(scene.to_arrays().xy[:, k]) for k in range(4)),
-                               np.ascontiguousarray(scene.to_arrays().kind)),
+    om = orc.Mesh(orc.RawScene(*(np.ascontiguousarray(sa.xy[:, k]) for k in range(4)),
+                               np.ascontiguousarray(sa.kind)),
                   orc.RawTri(np.ascontiguousarray(arr.vxy[:, 0]), np.ascontiguousarray(arr.vxy[:, 1]),
                              np.ascontiguousarray(arr.v), np.ascontiguousarray(arr.nbr),
                              np.ascontiguousarray(arr.flag)))
-    ref = om.trace(np.array([[0.0, 0.37, 1.0, 0.0]]))
-    assert s1 == ref["start"][0] and st1.tri_steps == ref["steps"][0]
-    assert (h1 is None and ref["seg"][0] < 0) or (h1.seg == ref["seg"][0] and h1.t == ref["t"][0])
-    assert (st1.tri_steps, getattr(h1, "t", None)) != (st0.tri_steps, getattr(h0, "t", None))
+    ref = om.trace(rays)
+    for k in ("start", "seg", "steps"):
+        assert np.array_equal(after[k], ref[k]), k
+    assert not np.array_equal(before["steps"], after["steps"])  # the edit is visible
+    assert accel.pack(tri) is p1  # unchanged content: the cache holds
 
 
 def test_kd_from_given_start_leaves():
