@@ -109,7 +109,9 @@ int mwt_device_count(int *count);
  * (16 B per triangle) when that fits, else walks the 32-B records from
  * global memory with the boundary table staged (896 threads); variant 3 tries
  * the per-triangle table first (A/B); variant 1 always
- * walks from global memory with 256-thread CTAs, `min_blocks_per_sm` CTAs per SM. */
+ * walks from global memory with 256-thread CTAs, `min_blocks_per_sm` CTAs per SM.
+ * With variant 2 or 3, `min_blocks_per_sm` only sizes the record-table CTA:
+ * the per-triangle and global-record paths always use 896-thread CTAs. */
 int mwt_set_tuning(int refill_below, int min_blocks_per_sm, int variant);
 
 /* Measurement helper (no reference counterpart): L2 read bandwidth of

@@ -21,6 +21,7 @@ unchanged.
 from __future__ import annotations
 
 import math
+import operator
 import weakref
 from dataclasses import dataclass
 from typing import Callable, Iterable, Optional
@@ -135,35 +136,34 @@ class _Packed:
         self.scene = scene
 
 
-def _segments_of(scene) -> list:
+def _segment_of(scene, sid: int):
+    """Scene segment ``sid`` (a reference Scene or this package's SceneArrays)."""
     if isinstance(scene, SceneArrays):
         from .geometry import Segment, SegmentKind
-        return [Segment(Point(*r[:2]), Point(*r[2:]),
-                        SegmentKind.GEOMETRY if k == 0 else SegmentKind.BOUNDARY)
-                for r, k in zip(scene.xy.tolist(), scene.kind.tolist())]
-    return list(scene.segments)
+        r = scene.xy[sid].tolist()
+        return Segment(Point(*r[:2]), Point(*r[2:]),
+                       SegmentKind.GEOMETRY if int(scene.kind[sid]) == 0 else SegmentKind.BOUNDARY)
+    return scene.segments[sid]
 
 
 # The reference edits triangulations in place (trimesh.flip_edge, the
 # annealer's vertex moves) and its walk reads the live mesh, so a cached pack
 # is reused only while the mesh's content is unchanged: every call compares a
-# fingerprint of the vertex coordinates, triangle corners, neighbours, flags
-# and the scene's segments (O(triangles) host work).  Set CHECK_MUTATION =
-# False for meshes known to be immutable, or call invalidate(tri) after an edit.
+# value snapshot of the vertex coordinates, triangle corners, neighbours and
+# flags, and the scene's (immutable) segments, with the one taken at packing
+# time (O(triangles) host work, ~50 us for a 200-triangle mesh).  Set
+# CHECK_MUTATION = False for meshes known to be immutable, or call
+# invalidate(tri) after an edit.
 CHECK_MUTATION = True
+_XY = operator.attrgetter("x", "y")
 
 
-def _fingerprint(tri) -> bytes:
-    import hashlib
-    h = hashlib.blake2b(digest_size=16)
-    h.update(np.array([(v.x, v.y) for v in tri.verts], dtype=np.float64).tobytes())
-    h.update(np.array([(-1,) * 9 if t is None else
-                       (*t.v, *[-1 if n is None else n for n in t.nbr], *t.flag) for t in tri.tris],
-                      dtype=np.int64).tobytes())
-    segs = tri.scene.segments
-    h.update(np.array([(s.a.x, s.a.y, s.b.x, s.b.y) for s in segs], dtype=np.float64).tobytes())
-    h.update(bytes(_kind(s) == "G" for s in segs))
-    return h.digest()
+def _fingerprint(tri) -> tuple:
+    """Value snapshot of everything the walk reads (copies, not references:
+    the reference mutates Tri.v / nbr / flag lists in place)."""
+    return (list(map(_XY, tri.verts)),
+            [None if t is None else (*t.v, *t.nbr, *t.flag) for t in tri.tris],
+            list(tri.scene.segments))
 
 
 def invalidate(obj) -> None:
@@ -198,10 +198,10 @@ def _ray_array(rays) -> np.ndarray:
                     dtype=np.float64).reshape(-1, 4)
 
 
-def _hit(segments, seg: int, t: float, u: float) -> Optional[Hit]:
+def _hit(scene, seg: int, t: float, u: float) -> Optional[Hit]:
     if seg < 0:
         return None
-    return Hit(int(seg), float(t), segments[int(seg)].point_at(float(u)))
+    return Hit(int(seg), float(t), _segment_of(scene, int(seg)).point_at(float(u)))
 
 
 # ----------------------------------------------------------------------
@@ -210,7 +210,7 @@ def _hit(segments, seg: int, t: float, u: float) -> Optional[Hit]:
 def trace_batch(tri, rays, start=None, device: int = 0) -> dict:
     """Every ray through ``tri``: start triangles located on the device unless
     given.  Returns numpy arrays start/seg/t/u/steps/status (reference ids)."""
-    P = pack(tri, device)
+    P = tri if isinstance(tri, _Packed) else pack(tri, device)
     r = _ray_array(rays)
     s = None
     if start is not None:
@@ -240,12 +240,12 @@ def traverse_triangulation(tri, ray: Ray, start_tri: int, index=None
     """accel.py:138-213 on the device.  Raises TraversalError exactly where the
     reference does (revisited state or no exit edge)."""
     P = pack(tri)
-    out = trace_batch(tri, _ray_array([ray]), [start_tri])
+    out = trace_batch(P, _ray_array([ray]), [start_tri])
     st = int(out["status"][0])
     if st & (_lib.ST_ERROR | _lib.ST_OVERFLOW):
         raise TraversalError(f"traversal failed from triangle {start_tri} (status {st:#x})")
     stats = TraversalStats(tri_steps=int(out["steps"][0]))
-    return _hit(_segments_of(P.scene), int(out["seg"][0]), out["t"][0], out["u"][0]), stats
+    return _hit(P.scene, int(out["seg"][0]), out["t"][0], out["u"][0]), stats
 
 
 class TriLocator:
@@ -399,7 +399,7 @@ def bvh_intersect(bvh, ray: Ray) -> tuple[Optional[Hit], TraversalStats]:
     if int(o["status"][0]) & _lib.ST_OVERFLOW:
         raise TraversalError("bvh stack overflow")
     stats = TraversalStats(bvh_node_tests=int(o["node_tests"][0]), bvh_prim_tests=int(o["prim_tests"][0]))
-    return _hit(_segments_of(bvh.scene), int(o["seg"][0]), o["t"][0], o["u"][0]), stats
+    return _hit(bvh.scene, int(o["seg"][0]), o["t"][0], o["u"][0]), stats
 
 
 def kd_intersect(kd, ray: Ray, start_leaf=None) -> tuple[Optional[Hit], TraversalStats]:
@@ -418,14 +418,14 @@ def kd_intersect(kd, ray: Ray, start_leaf=None) -> tuple[Optional[Hit], Traversa
         raise TraversalError("kd walk did not terminate")
     stats = TraversalStats(kd_nodes_visited=int(o["nodes"][0]), kd_rope_steps=int(o["ropes"][0]),
                            kd_prim_tests=int(o["prims"][0]))
-    return _hit(_segments_of(kd.scene), int(o["seg"][0]), o["t"][0], o["u"][0]), stats
+    return _hit(kd.scene, int(o["seg"][0]), o["t"][0], o["u"][0]), stats
 
 
 def brute_force_closest(scene, ray: Ray, index=None) -> Optional[Hit]:
     """accel.py:101-132 on the device."""
     m = _scene_mesh(scene)
     o = m.brute_force(_ray_array([ray]))
-    return _hit(_segments_of(scene), int(o["seg"][0]), o["t"][0], o["u"][0])
+    return _hit(scene, int(o["seg"][0]), o["t"][0], o["u"][0])
 
 
 @dataclass

@@ -42,33 +42,43 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, out_dir: str | None = None,
+          defines: list[str] | None = None) -> str:
+    """Build into _build/ (or ``out_dir``: an A/B variant with extra ``-D``
+    ``defines``, e.g. ab/<tag>/libmwt.so; never the shipped library)."""
+    out_dir = out_dir or OUT_DIR
+    lib = os.path.join(out_dir, "libmwt.so")
+    if out_dir == OUT_DIR and not defines and not force and up_to_date():
         return LIB
-    os.makedirs(OUT_DIR, exist_ok=True)
+    os.makedirs(out_dir, exist_ok=True)
+    extra = ["-D" + d for d in (defines or [])]
     objs = []
     for src in SOURCES:
-        obj = os.path.join(OUT_DIR, src + ".o")
-        cmd = [nvcc()] + flags() + ["-Xptxas", "-v", "-c", os.path.join(CSRC, src), "-o", obj] \
-            if src.endswith(".cu") else [nvcc()] + flags() + ["-c", os.path.join(CSRC, src), "-o", obj]
+        obj = os.path.join(out_dir, src + ".o")
+        cmd = [nvcc()] + flags() + extra + ["-Xptxas", "-v", "-c", os.path.join(CSRC, src), "-o", obj] \
+            if src.endswith(".cu") else [nvcc()] + flags() + extra + ["-c", os.path.join(CSRC, src), "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
             sys.stderr.write(r.stderr)
-        with open(os.path.join(OUT_DIR, src + ".ptxas.txt"), "w") as fh:
+        with open(os.path.join(out_dir, src + ".ptxas.txt"), "w") as fh:
             fh.write(r.stderr)
         objs.append(obj)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [nvcc()] + ARCH + ["-shared", "-ccbin", "/usr/bin/g++", "-o", tmp] + objs + ["-lcudart_static"]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("link failed")
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    # python build.py [--force] [-v] [--out DIR -DNAME[=V] ...]
+    a = sys.argv[1:]
+    out = a[a.index("--out") + 1] if "--out" in a else None
+    print(build(force="--force" in a, verbose="-v" in a, out_dir=out,
+                defines=[x[2:] for x in a if x.startswith("-D")]))

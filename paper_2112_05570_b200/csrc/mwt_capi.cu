@@ -81,6 +81,7 @@ struct mwt_mesh {
     std::mutex mu;
     void *scratch = nullptr;
     size_t scratch_bytes = 0;
+    long long *hist_scratch = nullptr;  // the sharded entry point's per-device histogram (under mu)
     cudaStream_t stream = nullptr;
 };
 
@@ -277,6 +278,7 @@ int mwt_mesh_destroy(mwt_mesh *m) {
     for (int k = 0; k < kHostStreams; k++)
         if (m->hstream[k]) cudaStreamDestroy(m->hstream[k]);
     if (m->scratch) cudaFree(m->scratch);
+    if (m->hist_scratch) cudaFree(m->hist_scratch);
     if (m->blob) cudaFree(m->blob);
     delete m;
     return MWT_OK;
@@ -651,9 +653,11 @@ int mwt_trace_generated_sharded(const mwt_mesh *const *meshes, int ndev, int mod
             const int64_t lo = shard_lo(n, ndev, k), cnt = shard_lo(n, ndev, k + 1) - lo;
             std::lock_guard<std::mutex> lk(m->mu);
             DeviceGuard g(m->device);
-            long long *dh = nullptr;
             cudaError_t e = g.ok ? cudaSuccess : cudaErrorInvalidDevice;
-            if (e == cudaSuccess) e = cudaMalloc(&dh, sizeof(long long) * MWT_HIST_LEN);
+            // allocated once per mesh handle, kept for later calls
+            if (e == cudaSuccess && !m->hist_scratch)
+                e = cudaMalloc(&m->hist_scratch, sizeof(long long) * MWT_HIST_LEN);
+            long long *dh = m->hist_scratch;
             if (e == cudaSuccess) e = cudaMemsetAsync(dh, 0, sizeof(long long) * MWT_HIST_LEN, m->stream);
             if (e == cudaSuccess && cnt > 0)
                 e = (cudaError_t)mwt::launch_trace_generated(m->dev, mode, box, seed, first + (uint64_t)lo,
@@ -662,7 +666,6 @@ int mwt_trace_generated_sharded(const mwt_mesh *const *meshes, int ndev, int mod
                 e = cudaMemcpyAsync(part[k].data(), dh, sizeof(long long) * MWT_HIST_LEN,
                                     cudaMemcpyDeviceToHost, m->stream);
             if (e == cudaSuccess) e = cudaStreamSynchronize(m->stream);
-            if (dh) cudaFree(dh);
             if (e != cudaSuccess) {
                 err[k].rc = MWT_E_CUDA;
                 err[k].msg = std::string("device ") + std::to_string(m->device) + ": " + cudaGetErrorName(e);

@@ -256,6 +256,15 @@ __device__ __forceinline__ void load_step(const MeshDev &M, uint32_t k, int4 &W,
 // test rather than sunk into the branch that consumes the words
 __device__ __forceinline__ void load_step_issue(const MeshDev &M, uint32_t k, int4 &W, double2 &A) {
     const int4 *p = M.step + 2 * (size_t)k;
+#ifdef MWT_SPLIT_LOAD
+    // A/B: the 24 used bytes as an 8-B and a 16-B load (the pad is not read)
+    uint32_t w0, w1;
+    asm volatile("ld.global.nc.v2.b32 {%0, %1}, [%2];" : "=r"(w0), "=r"(w1) : "l"(p));
+    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(A.x), "=d"(A.y) : "l"(p + 1));
+    W.x = (int)w0;
+    W.y = (int)w1;
+    W.z = W.w = 0;
+#else
     unsigned long long w01, w23;
     asm volatile("ld.global.nc.v4.b64 {%0, %1, %2, %3}, [%4];"
                  : "=l"(w01), "=l"(w23), "=d"(A.x), "=d"(A.y)
@@ -264,6 +273,7 @@ __device__ __forceinline__ void load_step_issue(const MeshDev &M, uint32_t k, in
     W.y = (int)(uint32_t)(w01 >> 32);
     W.z = (int)(uint32_t)w23;
     W.w = (int)(uint32_t)(w23 >> 32);
+#endif
 }
 
 // first triangle: edges 0 (s1,s2), 1 (s2,s0), 2 (s0,s1) in order, none skipped
@@ -1061,6 +1071,11 @@ __global__ void __launch_bounds__(kThreads) k_histogram(const int32_t *seg, cons
 
 #define MWT_LAUNCH_RET return (int)cudaGetLastError()
 
+// rays per k_trace launch: per-CTA ray offsets are 32-bit and the per-thread
+// hit / miss counters 21-bit (flushed once per launch), so even a one-CTA grid
+// (896 threads) stays in range; the launchers split larger calls
+constexpr int64_t kMaxLaunchRays = 1ll << 30;
+
 static int g_refill_below = 6;  // tuned on B200 (tools/breakdown.py): refill when <= 6 lanes still walk
 static int g_min_blocks = 4;    // register budget; see launch_k_trace_any
 static int g_variant = 2;       // 2: shared-memory staged walk when a compact table fits, else 1; 3: per-triangle table first
@@ -1180,24 +1195,40 @@ int launch_trace(const MeshDev &m, const double *rays, const int32_t *start, int
                  int32_t *o_start, int32_t *o_seg, double *o_t, double *o_u, int32_t *o_steps,
                  uint32_t *o_st, void *stream, int32_t *o_end) {
     if (n <= 0) return 0;
-    Launch L{};
-    L.src.rays = rays;
-    L.src.start = start;
-    L.out = TraceOut{o_start, o_seg, o_steps, o_t, o_u, o_st, o_end};
-    launch_k_trace_any<false>(m, L, n, nullptr, stream);
-    MWT_LAUNCH_RET;
+    // chunked so every launch keeps k_trace's 32-bit per-CTA ray offsets and
+    // 21-bit per-thread hit/miss counters in range (kMaxLaunchRays)
+    for (int64_t off = 0; off < n; off += kMaxLaunchRays) {
+        const int64_t c = n - off < kMaxLaunchRays ? n - off : kMaxLaunchRays;
+        auto at = [off](auto *p) { return p ? p + off : p; };
+        Launch L{};
+        L.src.rays = rays + 4 * off;
+        L.src.start = at(start);
+        L.out = TraceOut{at(o_start), at(o_seg), at(o_steps), at(o_t), at(o_u), at(o_st), at(o_end)};
+        launch_k_trace_any<false>(m, L, c, nullptr, stream);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return (int)e;
+    }
+    return 0;
 }
 
 int launch_trace_generated(const MeshDev &m, int mode, const double *box, uint64_t seed,
                            uint64_t first, int64_t n, int32_t *o_seg, double *o_t,
                            int32_t *o_steps, long long *hist, void *stream) {
     if (n <= 0) return 0;
-    Launch L{};
-    if (!make_raygen(mode, box, seed, L.src.gen)) return (int)cudaErrorInvalidValue;
-    L.src.first = first;
-    L.out = TraceOut{nullptr, o_seg, o_steps, o_t, nullptr, nullptr, nullptr};
-    launch_k_trace_any<true>(m, L, n, hist, stream);
-    MWT_LAUNCH_RET;
+    RayGen g;
+    if (!make_raygen(mode, box, seed, g)) return (int)cudaErrorInvalidValue;
+    for (int64_t off = 0; off < n; off += kMaxLaunchRays) {  // see launch_trace
+        const int64_t c = n - off < kMaxLaunchRays ? n - off : kMaxLaunchRays;
+        auto at = [off](auto *p) { return p ? p + off : p; };
+        Launch L{};
+        L.src.gen = g;
+        L.src.first = first + (uint64_t)off;
+        L.out = TraceOut{nullptr, at(o_seg), at(o_steps), at(o_t), nullptr, nullptr, nullptr};
+        launch_k_trace_any<true>(m, L, c, hist, stream);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return (int)e;
+    }
+    return 0;
 }
 
 int launch_histogram(const int32_t *seg, const int32_t *steps, const uint32_t *st, int64_t n,

@@ -531,9 +531,11 @@ def make_kdstart(nrays=2000):
         seg.append(-1 if h is None else h.seg); t.append(np.nan if h is None else h.t)
         nodes.append(st.kd_nodes_visited); ropes.append(st.kd_rope_steps); prims.append(st.kd_prim_tests)
         err.append(0)
-    out.update(seg=np.array(seg, np.int32), t=np.array(t), nodes=np.array(nodes, np.int32),
-               ropes=np.array(ropes, np.int32), prims=np.array(prims, np.int32), error=np.array(err, np.uint8))
-    print(f"kdstart: {nrays} rays, {int(np.sum(err))} errors, hits {int((out['seg'] >= 0).sum())}", flush=True)
+    # results under out_*: the flattened tree already owns `ropes` and `prims`
+    out.update(out_seg=np.array(seg, np.int32), out_t=np.array(t), out_nodes=np.array(nodes, np.int32),
+               out_ropes=np.array(ropes, np.int32), out_prims=np.array(prims, np.int32),
+               out_error=np.array(err, np.uint8))
+    print(f"kdstart: {nrays} rays, {int(np.sum(err))} errors, hits {int((out['out_seg'] >= 0).sum())}", flush=True)
     np.savez_compressed(os.path.join(HERE, "kdstart.npz"), **out)
 
 

@@ -113,7 +113,9 @@ def test_generated_kernel_equals_explicit_rays_and_histogram(cfg):
     ("lines1024", 6, 4, 3, 0), ("lines1024", 6, 4, 3, 1), ("lines64", 31, 4, 3, 0),
     ("lines1024", 0, 4, 2, 0), ("lines1024", 4, 4, 2, 0), ("lines1024", 31, 4, 2, 0), ("lines1024", 4, 4, 1, 0),
     ("lines1024", 6, 3, 2, 0), ("lines1024", 6, 2, 2, 0), ("floorplan64", 6, 4, 2, 0),
-    ("grass4096", 6, 4, 2, 0), ("grass4096", 6, 4, 3, 1)])  # nothing fits: 896-thread CTAs, all from L1/L2
+    ("grass4096", 6, 4, 2, 0), ("grass4096", 6, 4, 3, 1),
+    # variant 1: 256-thread CTAs from global memory, min_blocks 2 / 3 / 4
+    ("grass4096", 6, 2, 1, 0), ("grass4096", 6, 3, 1, 0), ("floorplan64", 6, 3, 1, 0)])  # nothing fits: 896-thread CTAs, all from L1/L2
 def test_tuning_knobs_do_not_change_results(cfg, refill, minb, variant, mode):
     from oracle import oracle as orc
     from paper_2112_05570_b200 import _lib
@@ -372,3 +374,22 @@ def test_single_process_sharded_entry_points(ndev):
     assert np.array_equal(a["t"][hit], b["t"][hit]) and np.array_equal(a["u"][hit], b["u"][hit])
     assert np.array_equal(histogram_host(b["seg"], b["steps"], b["status"])[:1027],
                           histogram_host(a["seg"], a["steps"], a["status"])[:1027])
+
+
+def test_binary_mesh_traces_like_the_text_mesh(tmp_path):
+    """mwt-mesh v1 (formats.save_mesh_binary) loaded by DeviceMesh.from_binary
+    walks exactly like the text fixture and the oracle."""
+    from oracle import oracle as orc
+    from paper_2112_05570_b200.engine import DeviceMesh
+    from paper_2112_05570_b200.formats import load_scene, load_tri, save_mesh_binary
+    paths = fixture_paths("hair512", "mwt")
+    save_mesh_binary(str(tmp_path / "m"), load_scene(paths[0]), load_tri(paths[1]))
+    mb = DeviceMesh.from_binary(str(tmp_path / "m"))
+    om = orc.Mesh.from_files(*paths)
+    for mode in (0, 1):
+        rays = orc.raygen(mode, (0, 0, 1, 1), 5, 0, 1 << 16)
+        got, ref = mb.trace(rays), om.trace(rays)
+        for k in ("start", "seg", "steps"):
+            assert np.array_equal(got[k], ref[k]), k
+        hit = ref["seg"] >= 0
+        assert np.array_equal(got["t"][hit], ref["t"][hit])

@@ -252,13 +252,13 @@ def test_kd_from_given_start_leaves():
     from paper_2112_05570_b200.engine import DeviceKd, DeviceMesh
     g = _golden("kdstart.npz")
     mesh = DeviceMesh.from_files(*fixture_paths("lines1024", "mwt"))
-    kd = DeviceKd(mesh, {k: g[k] for k in g.files})
+    kd = DeviceKd(mesh, {k: g[k] for k in g.files if not k.startswith("out_")})
     o = kd.trace(g["rays"], g["start"])
-    assert not (o["status"] & _lib.ST_ERROR).any() and not g["error"].any()
+    assert not (o["status"] & _lib.ST_ERROR).any() and not g["out_error"].any()
     for k in ("seg", "nodes", "ropes", "prims"):
-        assert np.array_equal(o[k], g[k]), k
-    hit = g["seg"] >= 0
-    assert np.array_equal(o["t"][hit], g["t"][hit])
+        assert np.array_equal(o[k], g["out_" + k]), k
+    hit = g["out_seg"] >= 0
+    assert np.array_equal(o["t"][hit], g["out_t"][hit])
     internal = int(np.nonzero(g["axis"] >= 0)[0][0])
     bad = kd.trace(g["rays"][:2], np.array([internal, -1], np.int32))
     assert (bad["status"] & _lib.ST_ERROR).all()

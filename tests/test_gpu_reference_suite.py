@@ -41,6 +41,11 @@ def test_reference_accel_and_acceptance_tests_through_the_drop_in():
         with open(os.path.join(log, "reference_suite.log"), "w") as fh:
             fh.write(out)
     assert r.returncode == 0, out[-6000:]
-    assert "mwt drop-in" in out
+    assert "mwt drop-in:" in out
+    # the reference tests really went through the drop-ins
+    line = [ln for ln in out.splitlines() if ln.startswith("mwt drop-in calls:")][-1]
+    calls = dict(kv.split("=") for kv in line.split(":", 1)[1].strip().split(", "))
+    for q in ("traverse_triangulation", "bvh_intersect", "kd_intersect"):
+        assert int(calls[q]) > 0, line
     for c in ("criterion 1", "criterion 8", "criterion 9", "criterion 10"):
         assert f"PASS {c}:" in out, c

@@ -2,7 +2,10 @@
 figures SURVEY.md 8d asks the bench to carry (instructions per ray and per
 step, branch efficiency, achieved L2 / DRAM GB/s, shared-memory wavefronts).
 
-usage: ncu_stats.py report.ncu-rep rays steps_sum > profiles/rNN_ncu_stats.json
+usage: ncu_stats.py report.ncu-rep rays steps_sum [workload order [libmwt.so]] > profiles/rNN_ncu_stats.json
+
+With workload/order the entry is keyed to the sha256 of the in-tree libmwt.so
+(the build that was captured), which is how bench.py finds it.
 """
 import csv
 import io
@@ -60,5 +63,17 @@ out = {
     "smem_bank_conflicts": g("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
     "local_memory_instructions": (g("sass__inst_executed_local_loads") or 0) +
     (g("sass__inst_executed_local_stores") or 0),
+    "l1_wavefronts": g("l1tex__data_pipe_lsu_wavefronts.sum"),
+    "l1_global_wavefronts": g("l1tex__data_pipe_lsu_wavefronts_mem_lg.sum") or
+    g("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum"),
+    "l1_wavefronts_per_step": (g("l1tex__data_pipe_lsu_wavefronts.sum") or 0) / steps,
+    "l1_hit_rate_pct": g("l1tex__t_sector_hit_rate.pct"),
 }
+if len(sys.argv) > 5:
+    import hashlib
+    import os
+    lib = sys.argv[6] if len(sys.argv) > 6 else os.path.join(
+        os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2112_05570_b200", "_build", "libmwt.so")
+    out["workload"], out["order"] = sys.argv[4], sys.argv[5]
+    out["lib_sha256"] = hashlib.sha256(open(lib, "rb").read()).hexdigest()
 print(json.dumps(out, indent=1))
