@@ -270,7 +270,12 @@ def roofline(args, hb, kms, clocks, sms, local):
          "hbm_algorithmic": {"achieved": achieved, "peak": hbm_pk, "unit": "GB/s", "frac": achieved / hbm_pk,
                              "peak_source": hbm_src,
                              "note": "the mesh is L2/L1/shared-memory resident; HBM carries only the "
-                                     "per-ray output, so this is not a binding roof"}}
+                                     "per-ray output, so this is not a binding roof"},
+         "l1_return_algorithmic": {"achieved": achieved, "peak": sms * 128 * sm_mhz / 1e3, "unit": "GB/s",
+                                   "frac": achieved / (sms * 128 * sm_mhz / 1e3),
+                                   "note": "the 32 B per step against the L1/shared-memory data path into the "
+                                           "registers: 128 B per SM per cycle at the sampled SM clock "
+                                           "(B300_MICROARCH.md smem/L1 crossbar)"}}
     cands = {}
     if st is not None and st.get("rays") == hb["rays"]:
         inst = st["warp_instructions"]

@@ -463,37 +463,57 @@ int mwt_bvh_create(const mwt_mesh *mesh, int32_t nnodes, const double *box, cons
         if (prims[k] < 0 || prims[k] >= mesh->dev.ns)
             return fail(MWT_E_INVALID, "bvh_create: primitive id out of range");
     DeviceGuard g(mesh->device);
-    std::vector<int32_t> child(2 * (size_t)nnodes), pr(2 * (size_t)nnodes);
-    for (int k = 0; k < nnodes; k++) {
-        child[2 * k] = left[k];
-        child[2 * k + 1] = right[k];
-        pr[2 * k] = prim_off[k];
-        pr[2 * k + 1] = prim_cnt[k];
+    // child refs and boxes in the parent's slots (mwt_internal.h BvhDev)
+    auto ref = [&](int c) { return left[c] < 0 ? ~c : c; };
+    const size_t nn = nnodes;
+    std::vector<double> cbox(8 * nn, 0.0);
+    std::vector<int32_t> cref(2 * nn, 0), pr(2 * nn, 0);
+    for (size_t k = 0; k < nn; k++) {
+        if (left[k] >= 0) {
+            const int c[2] = {left[k], right[k]};
+            for (int s = 0; s < 2; s++) {
+                cref[2 * k + s] = ref(c[s]);
+                for (int q = 0; q < 4; q++) cbox[8 * k + 4 * s + q] = box[4 * (size_t)c[s] + q];
+            }
+        } else {
+            pr[2 * k] = prim_off[k];
+            pr[2 * k + 1] = prim_cnt[k];
+        }
     }
     size_t np = nprims > 0 ? nprims : 1;
-    size_t bytes = Arena::align(32 * (size_t)nnodes) + 2 * Arena::align(8 * (size_t)nnodes) +
-                   Arena::align(4 * np);
+    size_t bytes = Arena::align(64 * nn) + 2 * Arena::align(8 * nn) + Arena::align(4 * np);
     Arena a;
     CK(cudaMalloc(&a.base, bytes));
     mwt_bvh *b = new mwt_bvh();
     b->mesh = mesh;
     b->blob = a.base;
-    double4 *dbox = carve<double4>(a, nnodes);
-    int2 *dch = carve<int2>(a, nnodes);
-    int2 *dpr = carve<int2>(a, nnodes);
+    double4 *dbox = carve<double4>(a, 2 * nn);
+    int2 *dref = carve<int2>(a, nn);
+    int2 *dpr = carve<int2>(a, nn);
     int32_t *dpm = carve<int32_t>(a, np);
-    cudaError_t e = cudaMemcpy(dbox, box, 32 * (size_t)nnodes, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(dch, child.data(), 8 * (size_t)nnodes, cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMemcpy(dpr, pr.data(), 8 * (size_t)nnodes, cudaMemcpyHostToDevice);
+    cudaError_t e = cudaMemcpy(dbox, cbox.data(), 64 * nn, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dref, cref.data(), 8 * nn, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dpr, pr.data(), 8 * nn, cudaMemcpyHostToDevice);
     if (e == cudaSuccess && nprims > 0) e = cudaMemcpy(dpm, prims, 4 * (size_t)nprims, cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         cudaFree(a.base);
         delete b;
         return cuda_fail(e, "bvh_create: upload");
     }
-    b->dev = mwt::BvhDev{nnodes, dbox, dch, dpr, dpm, a.base, (int32_t)bytes,
-                         (int32_t)((char *)dch - (char *)a.base), (int32_t)((char *)dpr - (char *)a.base),
-                         (int32_t)((char *)dpm - (char *)a.base)};
+    mwt::BvhDev d{};
+    d.nnodes = nnodes;
+    d.root = make_double4(box[0], box[1], box[2], box[3]);
+    d.root_ref = ref(0);
+    d.cbox = dbox;
+    d.cref = dref;
+    d.prange = dpr;
+    d.prims = dpm;
+    d.blob = a.base;
+    d.blob_bytes = (int32_t)bytes;
+    d.o_cref = (int32_t)((char *)dref - (char *)a.base);
+    d.o_prange = (int32_t)((char *)dpr - (char *)a.base);
+    d.o_prims = (int32_t)((char *)dpm - (char *)a.base);
+    b->dev = d;
     *out = b;
     return MWT_OK;
 }
@@ -540,49 +560,57 @@ int mwt_kd_create(const mwt_mesh *mesh, int32_t nnodes, int32_t num_leaves, cons
     for (int k = 0; k < nprims; k++)
         if (prims[k] < 0 || prims[k] >= mesh->dev.ns)
             return fail(MWT_E_INVALID, "kd_create: primitive id out of range");
+    for (int k = 0; k < nnodes; k++)
+        if (axis[k] < 0)
+            for (int s = 0; s < 4; s++)
+                if (rope_cost[4 * k + s] < 0 || rope_cost[4 * k + s] > 255)
+                    return fail(MWT_E_INVALID, "kd_create: rope cost out of range");
     DeviceGuard g(mesh->device);
-    std::vector<int32_t> child(2 * (size_t)nnodes), pr(2 * (size_t)nnodes);
-    for (int k = 0; k < nnodes; k++) {
-        child[2 * k] = left[k];
-        child[2 * k + 1] = right[k];
-        pr[2 * k] = prim_off[k];
-        pr[2 * k + 1] = prim_cnt[k];
+    // mwt_internal.h KdDev: 16-B node words, one 64-B record per leaf
+    const size_t nn = nnodes;
+    std::vector<int4> node(nn);
+    std::vector<mwt::KdLeaf> leaf;
+    for (size_t k = 0; k < nn; k++) {
+        if (axis[k] >= 0) {
+            unsigned long long pb;
+            std::memcpy(&pb, pos + k, 8);
+            node[k] = make_int4((int)(uint32_t)pb, (int)(uint32_t)(pb >> 32), left[k],
+                                (int)((uint32_t)right[k] | ((uint32_t)axis[k] << 31)));
+        } else {
+            node[k] = make_int4(0, 0, -1, (int)leaf.size());
+            uint32_t cost = 0;
+            for (int s = 0; s < 4; s++) cost |= (uint32_t)rope_cost[4 * k + s] << (8 * s);
+            mwt::KdLeaf L;
+            L.box = make_double4(box[4 * k], box[4 * k + 1], box[4 * k + 2], box[4 * k + 3]);
+            L.ropes = make_int4(ropes[4 * k], ropes[4 * k + 1], ropes[4 * k + 2], ropes[4 * k + 3]);
+            L.meta = make_int4(prim_off[k], prim_cnt[k], (int)cost, 0);
+            leaf.push_back(L);
+        }
     }
-    size_t np = nprims > 0 ? nprims : 1, nn = nnodes;
-    size_t bytes = Arena::align(4 * nn) + Arena::align(8 * nn) + Arena::align(8 * nn) +
-                   Arena::align(32 * nn) + 2 * Arena::align(16 * nn) + Arena::align(8 * nn) +
-                   Arena::align(4 * np);
+    const size_t nl = leaf.size() > 0 ? leaf.size() : 1;
+    size_t np = nprims > 0 ? nprims : 1;
+    size_t bytes = Arena::align(16 * nn) + Arena::align(sizeof(mwt::KdLeaf) * nl) + Arena::align(4 * np);
     Arena a;
     CK(cudaMalloc(&a.base, bytes));
     mwt_kd *k = new mwt_kd();
     k->mesh = mesh;
     k->blob = a.base;
-    int32_t *dax = carve<int32_t>(a, nn);
-    double *dpos = carve<double>(a, nn);
-    int2 *dch = carve<int2>(a, nn);
-    double4 *dbox = carve<double4>(a, nn);
-    int4 *drope = carve<int4>(a, nn);
-    int4 *dcost = carve<int4>(a, nn);
-    int2 *dpr = carve<int2>(a, nn);
+    int4 *dnode = carve<int4>(a, nn);
+    mwt::KdLeaf *dleaf = carve<mwt::KdLeaf>(a, nl);
     int32_t *dpm = carve<int32_t>(a, np);
     cudaError_t e = cudaSuccess;
     auto up = [&](void *dst, const void *src, size_t n) {
         if (e == cudaSuccess && n) e = cudaMemcpy(dst, src, n, cudaMemcpyHostToDevice);
     };
-    up(dax, axis, 4 * nn);
-    up(dpos, pos, 8 * nn);
-    up(dch, child.data(), 8 * nn);
-    up(dbox, box, 32 * nn);
-    up(drope, ropes, 16 * nn);
-    up(dcost, rope_cost, 16 * nn);
-    up(dpr, pr.data(), 8 * nn);
+    up(dnode, node.data(), 16 * nn);
+    up(dleaf, leaf.data(), sizeof(mwt::KdLeaf) * leaf.size());
     up(dpm, prims, 4 * (size_t)nprims);
     if (e != cudaSuccess) {
         cudaFree(a.base);
         delete k;
         return cuda_fail(e, "kd_create: upload");
     }
-    k->dev = mwt::KdDev{nnodes, num_leaves, dax, dpos, dch, dbox, drope, dcost, dpr, dpm};
+    k->dev = mwt::KdDev{nnodes, num_leaves, dnode, dleaf, dpm};  // guard: 4 * len(kd._leaves) + 16
     *out = k;
     return MWT_OK;
 }

@@ -325,7 +325,38 @@ __device__ __forceinline__ double side_of(const Ray &r, double2 v) {
     return r.dx * (v.y - r.oy) - r.dy * (v.x - r.ox);
 }
 
-// geometry.py:136-166
+// a / b correctly rounded from y = RN(1/b), so that several quotients by one
+// divisor cost one IEEE division: q = RN(a y) is within one ulp of a / b,
+// r = a - b q is exact (one FMA) and RN(q + r y) = RN(a / b) (Markstein's
+// theorem; round-to-nearest, no under- or overflow in any step).  The range
+// guards keep every step normal: |b|, |a| in [2^-400, 2^400] (or a = 0);
+// outside them the IEEE division itself.  Bit-identical to a / b.
+struct Rcp {
+    double b, y;
+    bool ok;
+};
+
+__device__ __forceinline__ Rcp make_rcp(double b) {
+    const double ab = fabs(b);
+    Rcp R;
+    R.b = b;
+    R.ok = ab >= 0x1p-400 && ab <= 0x1p400;
+    R.y = 1.0 / (R.ok ? b : 1.0);
+    return R;
+}
+
+__device__ __forceinline__ double div_rcp(double a, const Rcp &R) {
+    const double q = a * R.y;
+    const double r = __fma_rn(-q, R.b, a);
+    const double q1 = __fma_rn(r, R.y, q);
+    const double aa = fabs(a);
+    if (R.ok && (aa == 0.0 || (aa >= 0x1p-400 && aa <= 0x1p400))) return q1;
+    return a / R.b;
+}
+
+// geometry.py:136-166.  RCP: both quotients from one reciprocal (div_rcp);
+// the walk's epilogue keeps two IEEE divisions (fewer live registers there).
+template <bool RCP = true>
 __device__ __forceinline__ bool rsi(const Ray &r, double4 s, double &t, double &u, bool &par) {
     double ex = s.z - s.x, ey = s.w - s.y;
     double denom = r.dx * ey - r.dy * ex;
@@ -341,8 +372,16 @@ __device__ __forceinline__ bool rsi(const Ray &r, double4 s, double &t, double &
         if (ta <= tb) { t = ta; u = 0.0; } else { t = tb; u = 1.0; }
         return true;
     }
-    double tt = (wx * ey - wy * ex) / denom;
-    double uu = (wx * r.dy - wy * r.dx) / denom;
+    // (wx * ey - wy * ex) / denom and (wx * dy - wy * dx) / denom, one division
+    double tt, uu;
+    if (RCP) {
+        const Rcp R = make_rcp(denom);
+        tt = div_rcp(wx * ey - wy * ex, R);
+        uu = div_rcp(wx * r.dy - wy * r.dx, R);
+    } else {
+        tt = (wx * ey - wy * ex) / denom;
+        uu = (wx * r.dy - wy * r.dx) / denom;
+    }
     if (tt < 0.0 || uu < 0.0 || uu > 1.0) return false;
     t = tt;
     u = uu;
@@ -350,6 +389,7 @@ __device__ __forceinline__ bool rsi(const Ray &r, double4 s, double &t, double &
 }
 
 // accel.py:82-98 SceneIndex.canonical
+template <bool RCP = true>
 __device__ __forceinline__ int canonical(const MeshDev &M, const Ray &r, int sid, double t, double u, double &ot,
                          double &ou) {
     int best = sid;
@@ -364,7 +404,7 @@ __device__ __forceinline__ int canonical(const MeshDev &M, const Ray &r, int sid
             if (sid2 >= best) continue;
             double t2, u2;
             bool par = false;
-            if (!rsi(r, ldg4d(M.seg + sid2), t2, u2, par)) continue;
+            if (!rsi<RCP>(r, ldg4d(M.seg + sid2), t2, u2, par)) continue;
             if (fabs(t2 - t) <= tol) {
                 best = sid2;
                 bt = t2;

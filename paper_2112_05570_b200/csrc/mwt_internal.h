@@ -153,26 +153,34 @@ struct MeshDev {
     int32_t tri_seg_staged;  // ... and the segments fit after it
 };
 
+// K5 BVH (mwt_bvh_create).  A node visit reads both children's boxes and
+// refs from the parent's slots (no dependent load through a child index).
+// A ref is the child's node id if internal, ~node id if a leaf.
 struct BvhDev {
     int32_t nnodes;
-    const double4 *box;
-    const int2 *child;     // (left, right), left < 0 => leaf
-    const int2 *prange;    // (prim_off, prim_cnt)
+    double4 root;           // the root's box (the walk's first test)
+    int32_t root_ref;       // the root's ref
+    const double4 *cbox;    // [2n]: boxes of node n's left, right child (internal n)
+    const int2 *cref;       // [n]: refs of node n's left, right child (internal n)
+    const int2 *prange;     // [n]: (prim_off, prim_cnt) of leaf n
     const int32_t *prims;
-    // the four arrays as one blob (box at 0), for staging in shared memory
+    // the four arrays as one blob (cbox at 0), for staging in shared memory
     const void *blob;
-    int32_t blob_bytes, o_child, o_prange, o_prims;
+    int32_t blob_bytes, o_cref, o_prange, o_prims;
+};
+
+// K6 roped kd-tree (mwt_kd_create).  Node words by node id; one 64-B record
+// per leaf by leaf slot (the leaf's rank in node order).
+struct KdLeaf {
+    double4 box;
+    int4 ropes;  // rope target node ids per side (-1: none)
+    int4 meta;   // (prim_off, prim_cnt, rope cost of side s in bits 8s..8s+7, 0)
 };
 
 struct KdDev {
     int32_t nnodes, nleaves;
-    const int32_t *axis;
-    const double *pos;
-    const int2 *child;
-    const double4 *box;
-    const int4 *ropes;
-    const int4 *rope_cost;
-    const int2 *prange;
+    const int4 *node;     // internal: (pos lo, pos hi, left, right | axis << 31); leaf: (0, 0, -1, slot)
+    const KdLeaf *leaf;   // [nleaves]
     const int32_t *prims;
 };
 

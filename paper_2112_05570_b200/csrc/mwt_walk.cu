@@ -400,7 +400,7 @@ __device__ __forceinline__ int walk_terminal(const MeshDev &M, const Ray &r, con
     const double4 S = sseg ? sseg[sid] : ldg4d(M.seg + sid);
     double t, u;
     bool par = false;
-    bool ok = rsi(r, S, t, u, par);
+    bool ok = rsi<false>(r, S, t, u, par);
     if (par) st |= ST_PARALLEL;
     if (!ok) {
         // grazing numerical corner, accel.py:199-207
@@ -417,7 +417,7 @@ __device__ __forceinline__ int walk_terminal(const MeshDev &M, const Ray &r, con
         const double ex = S.z - S.x, ey = S.w - S.y;
         u = ((x - S.x) * ex + (y - S.y) * ey) / (ex * ex + ey * ey);  // Segment.param_of
     }
-    const int s2 = canonical(M, r, sid, t, u, ot, ou);
+    const int s2 = canonical<false>(M, r, sid, t, u, ot, ou);
     if (s2 != sid) st |= ST_CANON;
     return s2;
 }

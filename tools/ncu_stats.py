@@ -21,10 +21,21 @@ rows = [r for r in rows[2:] if len(r) == len(hdr) and "k_trace" in r[hdr.index("
 r = rows[0]
 
 
+def col(name):
+    """column of a metric (some sections prefix the name, e.g. SM_A.TriageCompute.)"""
+    if name in hdr:
+        return hdr.index(name)
+    for i, h in enumerate(hdr):
+        if h.endswith("." + name):
+            return i
+    return None
+
+
 def g(name):
-    if name not in hdr:
+    i = col(name)
+    if i is None:
         return None
-    v = r[hdr.index(name)].replace(",", "")
+    v = r[i].replace(",", "")
     try:
         return float(v)
     except ValueError:
@@ -43,6 +54,8 @@ def gb(name):  # a byte count in bytes, whatever unit ncu printed
 
 
 dram = gb("dram__bytes_read.sum") + gb("dram__bytes_write.sum")
+nsm = g("device__attribute_multiprocessor_count") or 148
+wf = g("l1tex__data_pipe_lsu_wavefronts.sum") or (g("l1tex__data_pipe_lsu_wavefronts.avg") or 0) * nsm
 out = {
     "report": rep.split("/")[-1],
     "kernel": r[hdr.index("Kernel Name")][:80],
@@ -63,11 +76,21 @@ out = {
     "smem_bank_conflicts": g("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"),
     "local_memory_instructions": (g("sass__inst_executed_local_loads") or 0) +
     (g("sass__inst_executed_local_stores") or 0),
-    "l1_wavefronts": g("l1tex__data_pipe_lsu_wavefronts.sum"),
-    "l1_global_wavefronts": g("l1tex__data_pipe_lsu_wavefronts_mem_lg.sum") or
-    g("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum"),
-    "l1_wavefronts_per_step": (g("l1tex__data_pipe_lsu_wavefronts.sum") or 0) / steps,
-    "l1_hit_rate_pct": g("l1tex__t_sector_hit_rate.pct"),
+    # L1 data-pipe wavefronts (global + local + shared), summed over the SMs
+    "l1_wavefronts": wf,
+    "l1_wavefronts_lgds": (g("l1tex__data_pipe_lsu_wavefronts_mem_lgds.avg") or 0) * nsm,
+    "l1_wavefronts_shared": g("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
+    "l1_wavefronts_pct_of_peak": g("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+    "l1_wavefronts_per_step": wf / steps if wf else None,
+    "global_load_requests": g("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum"),
+    "global_load_sector_hit_pct": g("l1tex__t_sector_pipe_lsu_mem_global_op_ld_hit_rate.pct"),
+    "lsu_writeback_active_pct": g("l1tex__lsu_writeback_active.avg.pct_of_peak_sustained_elapsed"),
+    "fp64_pipe_pct": g("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active"),
+    "stalls_per_issue": {k: g(f"smsp__average_warps_issue_stalled_{k}_per_issue_active.ratio")
+                         for k in ("wait", "long_scoreboard", "short_scoreboard", "not_selected",
+                                   "math_pipe_throttle", "branch_resolving", "dispatch_stall",
+                                   "no_instruction", "mio_throttle", "lg_throttle", "barrier")},
+    "sm_count": nsm,
 }
 if len(sys.argv) > 5:
     import hashlib
