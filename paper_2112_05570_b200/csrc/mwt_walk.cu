@@ -254,26 +254,30 @@ __device__ __forceinline__ void load_step(const MeshDev &M, uint32_t k, int4 &W,
 // the same record as ONE 256-bit load (sm_100 LDG.E.ENL2.256: one L1
 // wavefront per lane instead of two); volatile, so it is issued before the side
 // test rather than sunk into the branch that consumes the words
+template <bool SPLIT = false>
 __device__ __forceinline__ void load_step_issue(const MeshDev &M, uint32_t k, int4 &W, double2 &A) {
     const int4 *p = M.step + 2 * (size_t)k;
-#ifdef MWT_SPLIT_LOAD
-    // A/B: the 24 used bytes as an 8-B and a 16-B load (the pad is not read)
-    uint32_t w0, w1;
-    asm volatile("ld.global.nc.v2.b32 {%0, %1}, [%2];" : "=r"(w0), "=r"(w1) : "l"(p));
-    asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(A.x), "=d"(A.y) : "l"(p + 1));
-    W.x = (int)w0;
-    W.y = (int)w1;
-    W.z = W.w = 0;
-#else
-    unsigned long long w01, w23;
-    asm volatile("ld.global.nc.v4.b64 {%0, %1, %2, %3}, [%4];"
-                 : "=l"(w01), "=l"(w23), "=d"(A.x), "=d"(A.y)
-                 : "l"(p));
-    W.x = (int)(uint32_t)w01;
-    W.y = (int)(uint32_t)(w01 >> 32);
-    W.z = (int)(uint32_t)w23;
-    W.w = (int)(uint32_t)(w23 >> 32);
-#endif
+    if (SPLIT) {
+        // the 24 used bytes as an 8-B and a 16-B load (the pad is not read):
+        // 6 instead of 8 L1 data-pipe wavefronts per warp when the lanes'
+        // records are few (coherent rays), two wavefronts per lane when they
+        // are scattered
+        uint32_t w0, w1;
+        asm volatile("ld.global.nc.v2.b32 {%0, %1}, [%2];" : "=r"(w0), "=r"(w1) : "l"(p));
+        asm volatile("ld.global.nc.v2.f64 {%0, %1}, [%2];" : "=d"(A.x), "=d"(A.y) : "l"(p + 1));
+        W.x = (int)w0;
+        W.y = (int)w1;
+        W.z = W.w = 0;
+    } else {
+        unsigned long long w01, w23;
+        asm volatile("ld.global.nc.v4.b64 {%0, %1, %2, %3}, [%4];"
+                     : "=l"(w01), "=l"(w23), "=d"(A.x), "=d"(A.y)
+                     : "l"(p));
+        W.x = (int)(uint32_t)w01;
+        W.y = (int)(uint32_t)(w01 >> 32);
+        W.z = (int)(uint32_t)w23;
+        W.w = (int)(uint32_t)(w23 >> 32);
+    }
 }
 
 // first triangle: edges 0 (s1,s2), 1 (s2,s0), 2 (s0,s1) in order, none skipped
@@ -707,7 +711,7 @@ __device__ __forceinline__ void fetch_step(const MeshDev &M, const uint2 *srec, 
         wy = X.y;
     } else {
         int4 W;
-        load_step_issue(M, k, W, A);
+        load_step_issue<TRI>(M, k, W, A);  // (TRI without SMEM: split loads)
         wx = (uint32_t)W.x;
         wy = (uint32_t)W.y;
     }
@@ -773,7 +777,9 @@ __device__ __forceinline__ void bulk_stage(unsigned long long *bar, int n, void 
 // otherwise the tight loop reads the 32-B step records from global memory.
 // TRI (with SMEM): the per-triangle compact table is staged instead of the
 // per-record one (meshes too large for the latter); locate and the
-// first-triangle words then read global memory.
+// first-triangle words then read global memory.  TRI without SMEM: the
+// global step records are read as 8 + 16 B (load_step_issue<true>; chosen
+// for the coherent generator orders, FloorPlan +3%, iid orders -18%).
 template <bool GEN, int MINB, int THREADS, bool SMEM, bool STAGE = SMEM, bool TRI = false>
 __global__ void __launch_bounds__(THREADS, MINB)
     k_trace(const __grid_constant__ MeshDev M, const __grid_constant__ Launch L, long long n,
@@ -1160,6 +1166,10 @@ static void launch_k_trace_any(const MeshDev &m, const Launch &L, long long n, l
     // the per-triangle compact table when the record table does not fit
     if (g_variant >= 2 && launch_k_trace<GEN, 1, 896, true, true, true>(m, L, n, hist, stream)) return;
     // global walk records; boundary table (and segments when they fit) staged
+    if constexpr (GEN) {
+        if (g_variant >= 2 && L.src.gen.cmask && launch_k_trace<true, 1, 896, false, true, true>(m, L, n, hist, stream))
+            return;
+    }
     if (g_variant >= 2 && launch_k_trace<GEN, 1, 896, false, true>(m, L, n, hist, stream)) return;
     // nothing fits shared memory (Grass-4096's 4,108-edge boundary table): the
     // same 896-thread persistent CTAs reading every table from L1/L2
