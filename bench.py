@@ -27,7 +27,6 @@ bounded sample of the same workload.
 from __future__ import annotations
 
 import argparse
-import hashlib
 import json
 import os
 import subprocess
@@ -224,15 +223,15 @@ def run_reference_arm(args, world: int, rank: int):
     print(json.dumps(line), flush=True)
 
 
-def lib_sha256() -> str:
+def lib_build_id() -> str:
     from paper_2112_05570_b200 import _lib
-    with open(_lib.LIB_PATH, "rb") as fh:
-        return hashlib.sha256(fh.read()).hexdigest()
+    return _lib.lib.mwt_build_id().decode()
 
 
-def ncu_stats_for(workload: str, order: str, sha: str):
+def ncu_stats_for(workload: str, order: str, bid: str):
     """The committed ncu figures of this build's dominant launch, if a capture
-    of exactly this library (sha256) and workload exists (profiles/r*_ncu_stats.json)."""
+    of exactly this build (mwt_build_id: sources + flags) and workload exists
+    (profiles/r*_ncu_stats.json)."""
     pdir = os.path.join(ROOT, "profiles")
     for f in sorted(os.listdir(pdir), reverse=True):
         if not f.endswith("_ncu_stats.json"):
@@ -240,7 +239,7 @@ def ncu_stats_for(workload: str, order: str, sha: str):
         with open(os.path.join(pdir, f)) as fh:
             d = json.load(fh)
         for e in (d if isinstance(d, list) else [d]):
-            if e.get("lib_sha256") == sha and e.get("workload") == workload and e.get("order") == order:
+            if e.get("build_id") == bid and e.get("workload") == workload and e.get("order") == order:
                 return dict(e, file=f)
     return None
 
@@ -261,7 +260,7 @@ def roofline(args, hb, kms, clocks, sms, local):
         l2pk, l2src = l2_peak_file(), f"profiles/r01_l2_peak.json ({e})"
     sm_mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
     wl = f"{args.config}/{args.mesh}"
-    st = ncu_stats_for(wl, args.order, lib_sha256())
+    st = ncu_stats_for(wl, args.order, lib_build_id())
     r = {"kernel": "k_trace (mwt_trace_generated_dev, largest ray part)", "kernel_ms": kms,
          "algo_bytes_per_launch": algo,
          "algo_bytes_rule": "32 B per triangle step (one step record: 2 exit words + apex corner)",
@@ -289,7 +288,7 @@ def roofline(args, hb, kms, clocks, sms, local):
                                      "note": "L1 data pipe (global + shared): one wavefront per SM per cycle"}
         for c in cands.values():
             c["frac"] = c["achieved"] / c["peak"]
-        r["ncu_capture"] = {k: st.get(k) for k in ("file", "report", "lib_sha256", "warp_instructions",
+        r["ncu_capture"] = {k: st.get(k) for k in ("file", "report", "build_id", "warp_instructions",
                                                      "l1_wavefronts", "dram_bytes", "duration_ms")}
         r["traffic"] = st.get("dram_bytes")
     else:

@@ -99,6 +99,11 @@ typedef struct {
 /* Library / error plumbing */
 int mwt_abi_version(void);
 const char *mwt_last_error(void);
+
+/* Identity of this build: sha256 (hex, first 16 bytes) of the kernel and ABI
+ * sources and the nvcc flags they were compiled with -- profiles captured with
+ * ncu are keyed to it (bench.py). */
+const char *mwt_build_id(void);
 int mwt_device_count(int *count);
 /* Tuning knobs of the persistent walk kernel (process-wide; -1 = keep).
  * Lanes whose rays ended refill in one batch once at most `refill_below`

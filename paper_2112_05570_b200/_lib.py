@@ -71,6 +71,7 @@ I32, I64, U64, INT = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_i
 SIGNATURES = {
     "mwt_abi_version": (INT, []),
     "mwt_last_error": (ctypes.c_char_p, []),
+    "mwt_build_id": (ctypes.c_char_p, []),
     "mwt_device_count": (INT, [P]),
     "mwt_probe_l2_read": (INT, [INT, I64, INT, P]),
     "mwt_set_tuning": (INT, [INT, INT, INT]),

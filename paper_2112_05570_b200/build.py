@@ -42,6 +42,20 @@ def up_to_date() -> bool:
     return all(os.path.getmtime(d) <= t for d in deps)
 
 
+def build_id(defines: list[str] | None = None) -> str:
+    """sha256 of the sources, headers, flags and defines (deterministic, unlike
+    the linked binary): mwt_build_id() of the library built from them."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in SOURCES + ["mwt_internal.h", "mwt_device.cuh"]:
+        with open(os.path.join(CSRC, f), "rb") as fh:
+            h.update(f.encode() + b"\0" + fh.read())
+    with open(os.path.join(ROOT, "include", "mwt.h"), "rb") as fh:
+        h.update(fh.read())
+    h.update(" ".join(flags() + sorted(defines or [])).replace(ROOT, "").encode())
+    return h.hexdigest()[:32]
+
+
 def build(force: bool = False, verbose: bool = False, out_dir: str | None = None,
           defines: list[str] | None = None) -> str:
     """Build into _build/ (or ``out_dir``: an A/B variant with extra ``-D``
@@ -51,7 +65,7 @@ def build(force: bool = False, verbose: bool = False, out_dir: str | None = None
     if out_dir == OUT_DIR and not defines and not force and up_to_date():
         return LIB
     os.makedirs(out_dir, exist_ok=True)
-    extra = ["-D" + d for d in (defines or [])]
+    extra = ["-D" + d for d in (defines or [])] + [f'-DMWT_BUILD_ID="{build_id(defines)}"']
     objs = []
     for src in SOURCES:
         obj = os.path.join(out_dir, src + ".o")

@@ -108,6 +108,11 @@ int mwt_set_tuning(int refill_below, int min_blocks_per_sm, int variant) {
 
 const char *mwt_last_error(void) { return g_err.c_str(); }
 
+#ifndef MWT_BUILD_ID
+#define MWT_BUILD_ID "unknown"
+#endif
+const char *mwt_build_id(void) { return MWT_BUILD_ID; }
+
 int mwt_probe_l2_read(int device, int64_t bytes, int passes, double *gbs_out) {
     if (!gbs_out || bytes < (1 << 20) || bytes > (int64_t(1) << 30) || passes < 1 || passes > 100000)
         return fail(MWT_E_INVALID, "probe_l2_read: bad argument");

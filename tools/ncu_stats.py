@@ -2,10 +2,10 @@
 figures SURVEY.md 8d asks the bench to carry (instructions per ray and per
 step, branch efficiency, achieved L2 / DRAM GB/s, shared-memory wavefronts).
 
-usage: ncu_stats.py report.ncu-rep rays steps_sum [workload order [libmwt.so]] > profiles/rNN_ncu_stats.json
+usage: ncu_stats.py report.ncu-rep rays steps_sum [workload order [build_id]] > profiles/rNN_ncu_stats.json
 
-With workload/order the entry is keyed to the sha256 of the in-tree libmwt.so
-(the build that was captured), which is how bench.py finds it.
+With workload/order the entry is keyed to the captured build's
+mwt_build_id(), which is how bench.py finds it.
 """
 import csv
 import io
@@ -93,10 +93,11 @@ out = {
     "sm_count": nsm,
 }
 if len(sys.argv) > 5:
-    import hashlib
+    # keyed to the build it captured: mwt_build_id() (sources + flags; argv[6]
+    # overrides, default: the build id of the sources in this tree)
     import os
-    lib = sys.argv[6] if len(sys.argv) > 6 else os.path.join(
-        os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2112_05570_b200", "_build", "libmwt.so")
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2112_05570_b200 import build as _b
     out["workload"], out["order"] = sys.argv[4], sys.argv[5]
-    out["lib_sha256"] = hashlib.sha256(open(lib, "rb").read()).hexdigest()
+    out["build_id"] = sys.argv[6] if len(sys.argv) > 6 else _b.build_id()
 print(json.dumps(out, indent=1))
