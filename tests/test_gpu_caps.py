@@ -104,3 +104,44 @@ def test_drop_in_raises_where_the_device_overflows(monkeypatch):
         accel.kd_intersect(fk, ray)
     with pytest.raises(accel.TraversalError):
         accel.bvh_intersect(fb, ray)
+
+
+def _square_fan(k):
+    """k triangles fanned from (0.5, 0.5) to k points along the unit square's
+    boundary (CCW, corners included): every triangle contains the centre."""
+    from paper_2112_05570_b200.formats import SceneArrays, TriArrays
+    per = k // 4
+    pts = []
+    for a, b in (((0, 0), (1, 0)), ((1, 0), (1, 1)), ((1, 1), (0, 1)), ((0, 1), (0, 0))):
+        for j in range(per):
+            f = j / per
+            pts.append((a[0] + (b[0] - a[0]) * f, a[1] + (b[1] - a[1]) * f))
+    b = np.array(pts)
+    n = len(b)
+    vxy = np.vstack([[0.5, 0.5], b])
+    v = np.array([[0, 1 + i, 1 + (i + 1) % n] for i in range(n)], np.int32)
+    nbr = np.array([[-1, (i + 1) % n, (i - 1) % n] for i in range(n)], np.int32)
+    flag = np.array([[i, -1, -1] for i in range(n)], np.int32)
+    xy = np.array([[*b[i], *b[(i + 1) % n]] for i in range(n)])
+    return SceneArrays(xy, np.ones(n, np.uint8)), TriArrays(vxy, v, nbr, flag)
+
+
+@pytest.mark.parametrize("k", [100, 160, 164, 200])
+def test_locate_flood_cap(k):
+    """kFloodCap = 160 triangles in the lowest-id tie flood (accel.py:226-238):
+    a point shared by k triangles (a k-triangle fan's centre)."""
+    from oracle import oracle as orc
+    from paper_2112_05570_b200 import _lib
+    from paper_2112_05570_b200.engine import DeviceMesh
+    sc, tri = _square_fan(k)
+    om = orc.Mesh(orc.RawScene(*(np.ascontiguousarray(sc.xy[:, q]) for q in range(4)), sc.kind),
+                  orc.RawTri(np.ascontiguousarray(tri.vxy[:, 0]), np.ascontiguousarray(tri.vxy[:, 1]),
+                             tri.v, tri.nbr, tri.flag))
+    pts = np.array([[0.5, 0.5], [0.3, 0.2], [0.5, 0.9]])
+    rid, rst = om.locate(pts)
+    tid, st = DeviceMesh(sc, tri).locate(pts)
+    assert np.array_equal(tid[1:], rid[1:])
+    if k <= 160:
+        assert tid[0] == rid[0] == 0 and not (st[0] & _lib.ST_OVERFLOW)
+    else:
+        assert rid[0] == 0 and (st[0] & _lib.ST_OVERFLOW)
