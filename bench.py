@@ -46,6 +46,9 @@ CONFIGS = {
     "grass4096": ((0.0, 0.0, 1.0, 0.5), [(0, 1 << 24)]),
     "hair512": ((0.0, 0.0, 1.0, 1.0), [(0, 1 << 24)]),
     "floorplan64": ((0.0, 0.0, 1.0, 1.0), [(0, 1 << 26)]),
+    # Grass / Hair under the other crossing policies (fixtures/gen_fixtures.py)
+    "grass4096l": ((0.0, 0.0, 1.0, 0.5), [(0, 1 << 24)]),
+    "hair512r": ((0.0, 0.0, 1.0, 1.0), [(0, 1 << 24)]),
 }
 SEED = 0
 ALGO_BYTES_PER_STEP = 32  # 16-B link record + 16-B apex corner per triangle step

@@ -231,6 +231,89 @@ def scene_hair(n: int, seed: int, name: str) -> Scene:
                             f"policy=cut-at-first-contact, strands_kept={strands})")
 
 
+def scene_grass_lanes(n: int, seed: int, name: str) -> Scene:
+    """Grass-4096 with the reference gen_grass's crossing policy (lane
+    confinement, generators.py:113-131): blade k is rooted in lane
+    [k/n, (k+1)/n] (x0 uniform in its inner 80%) and every vertex's x is
+    clamped to the lane minus a 6% pad, so no two blades can touch and every
+    blade keeps its 4 segments; height, base lean N(0, 15 deg) and per-segment
+    bend N(0, 5 deg) as the recipe (equal segment lengths before the clamp)."""
+    rng = np.random.default_rng(seed)
+    h = SegHash(0.02)
+    lane = 1.0 / n
+    for k in range(n):
+        lo, hi = k * lane, (k + 1) * lane
+        pad = 0.06 * lane
+        x0 = float(rng.uniform(lo + 0.1 * lane, hi - 0.1 * lane))
+        height = float(rng.uniform(0.1, 0.4))
+        lean = float(rng.normal(0.0, math.radians(15.0)))
+        bends = rng.normal(0.0, math.radians(5.0), size=3)
+        step = height / 4.0
+        p = Point(x0, 0.0)
+        phi = lean
+        for q in range(4):
+            if q > 0:
+                phi += float(bends[q - 1])
+            nx = min(max(p.x + step * math.sin(phi), lo + pad), hi - pad)
+            b = Point(nx, p.y + step * abs(math.cos(phi)))
+            seg = Segment(p, b)
+            if h.crosses(seg):  # (cannot happen: lanes are disjoint and y grows)
+                raise RuntimeError(f"{name}: blade {k} crosses")
+            h.add(seg)
+            p = b
+    return Scene(h.segs + unit_square_boundary(), name=name,
+                 provenance=f"fixtures/gen_fixtures.py scene_grass_lanes(n={n}, seed={seed}, "
+                            f"policy=lane-confinement (reference gen_grass), blades_kept={n})")
+
+
+def scene_hair_resample(n: int, seed: int, name: str, tries: int = 32) -> Scene:
+    """Hair-512 with a resampling crossing policy: a strand step whose segment
+    would touch placed geometry redraws its turning angle (N(0, 10 deg) added
+    to the current heading) up to `tries` times, as the reference gen_lines
+    redraws a crossing segment (generators.py:71-89); only when every draw
+    touches is the step cut at its first contact and the strand ended (the
+    policy of scene_hair).  A step leaving the unit square is clipped and ends
+    the strand."""
+    rng = np.random.default_rng(seed)
+    h = SegHash(0.02)
+    strands = 0
+    for _ in range(n):
+        alpha = float(rng.uniform(0.0, 2.0 * math.pi))
+        p = Point(0.5 + 0.3 * math.cos(alpha), 0.5 + 0.3 * math.sin(alpha))
+        heading = alpha
+        added = 0
+        for k in range(32):
+            seg, end = None, False
+            for t in range(tries):
+                hd = heading + (float(rng.normal(0.0, math.radians(10.0))) if k > 0 else 0.0)
+                b = Point(p.x + 0.01 * math.cos(hd), p.y + 0.01 * math.sin(hd))
+                if not (0.0 <= b.x <= 1.0 and 0.0 <= b.y <= 1.0):
+                    clipped = _clip_unit_square(p, b)
+                    if clipped is None or clipped[0] != p:
+                        break
+                    b, end = clipped[1], True
+                cand = Segment(p, b)
+                if cand.length >= 1e-6 and not h.crosses(cand):
+                    seg, heading = cand, hd
+                    break
+                end = False
+            if seg is None:
+                # every draw touches: cut the last draw at its first contact (scene_hair's rule)
+                n_before = len(h.segs)
+                _grow(h, iter([p, Point(p.x + 0.01 * math.cos(heading), p.y + 0.01 * math.sin(heading))]))
+                added += len(h.segs) - n_before
+                break
+            h.add(seg)
+            added += 1
+            p = seg.b
+            if end:
+                break
+        strands += added > 0
+    return Scene(h.segs + unit_square_boundary(), name=name,
+                 provenance=f"fixtures/gen_fixtures.py scene_hair_resample(n={n}, seed={seed}, "
+                            f"policy=resample-turn x{tries} then cut-at-first-contact, strands_kept={strands})")
+
+
 def scene_floorplan(n: int, seed: int, name: str) -> Scene:
     rng = np.random.default_rng(seed)
     ang = math.radians(30.0)
@@ -294,6 +377,18 @@ CONFIGS = {
         box=(0.0, 0.0, 1.0, 0.5), rays=1 << 24, structures=True),
     "hair512": dict(
         scene=lambda: scene_hair(512, 0, "hair512"),
+        pipeline=dict(levels=4, steps_per_level=200, iterations=1,
+                      angle_grid=[0.0], area_grid=[math.inf]),
+        box=(0.0, 0.0, 1.0, 1.0), rays=1 << 24, structures=True),
+    # the two recipes above under the other crossing policies:
+    # every blade keeps its 4 segments / strands steer around contacts
+    "grass4096l": dict(
+        scene=lambda: scene_grass_lanes(4096, 0, "grass4096l"),
+        pipeline=dict(levels=4, steps_per_level=200, iterations=1,
+                      angle_grid=[0.0], area_grid=[math.inf]),
+        box=(0.0, 0.0, 1.0, 0.5), rays=1 << 24, structures=True),
+    "hair512r": dict(
+        scene=lambda: scene_hair_resample(512, 0, "hair512r"),
         pipeline=dict(levels=4, steps_per_level=200, iterations=1,
                       angle_grid=[0.0], area_grid=[math.inf]),
         box=(0.0, 0.0, 1.0, 1.0), rays=1 << 24, structures=True),

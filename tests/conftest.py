@@ -9,8 +9,10 @@ if ROOT not in sys.path:
 
 FIXTURES = os.path.join(ROOT, "fixtures", "data")
 GOLDEN = os.path.join(ROOT, "tests", "golden")
-CONFIGS = ["lines64", "lines1024", "grass4096", "hair512", "floorplan64"]
-BOXES = {"grass4096": (0.0, 0.0, 1.0, 0.5)}
+# BASELINE.json configs[0..4], then Grass / Hair under the other crossing
+# policies (fixtures/gen_fixtures.py: lane confinement, turn resampling)
+CONFIGS = ["lines64", "lines1024", "grass4096", "hair512", "floorplan64", "grass4096l", "hair512r"]
+BOXES = {"grass4096": (0.0, 0.0, 1.0, 0.5), "grass4096l": (0.0, 0.0, 1.0, 0.5)}
 
 
 def pytest_configure(config):

@@ -48,6 +48,8 @@ PARTS = {
     "grass4096": ((0.0, 0.0, 1.0, 0.5), [(0, 1 << 24)]),
     "hair512": ((0.0, 0.0, 1.0, 1.0), [(0, 1 << 24)]),
     "floorplan64": ((0.0, 0.0, 1.0, 1.0), [(0, 1 << 26)]),
+    "grass4096l": ((0.0, 0.0, 1.0, 0.5), [(0, 1 << 24)]),
+    "hair512r": ((0.0, 0.0, 1.0, 1.0), [(0, 1 << 24)]),
 }
 sys.path.insert(0, os.path.dirname(HERE))
 from digests import digest_start, digest_walk  # noqa: E402  (tests/digests.py, shared with the tests)
@@ -161,7 +163,16 @@ def main():
             cd["parts"].append({"mode": base, "n": total, "chunks": chunks})
         if complete:
             final["configs"][cfg] = cd
-    with open(os.path.join(HERE, f"digests_{a.mesh}.json"), "w") as fh:
+    # configs recorded by an earlier run (whose partial file is gone) are kept
+    fpath = os.path.join(HERE, f"digests_{a.mesh}.json")
+    if os.path.exists(fpath):
+        with open(fpath) as fh:
+            old = json.load(fh)
+        if old.get("chunk") == CHUNK and old.get("seed") == SEED:
+            for cfg, cd in old["configs"].items():
+                final["configs"].setdefault(cfg, cd)
+    final["configs"] = {c: final["configs"][c] for c in PARTS if c in final["configs"]}
+    with open(fpath, "w") as fh:
         json.dump(final, fh, separators=(",", ":"))
     print("configs complete:", sorted(final["configs"]), flush=True)
 

@@ -41,8 +41,8 @@ from conftest import random_segment_scene  # noqa: E402  (reference tests/confte
 
 from oracle.raygen import raygen  # noqa: E402
 
-CONFIGS = ["lines64", "lines1024", "grass4096", "hair512", "floorplan64"]
-BOXES = {"grass4096": (0.0, 0.0, 1.0, 0.5)}
+CONFIGS = ["lines64", "lines1024", "grass4096", "hair512", "floorplan64", "grass4096l", "hair512r"]
+BOXES = {"grass4096": (0.0, 0.0, 1.0, 0.5), "grass4096l": (0.0, 0.0, 1.0, 0.5)}
 FIX = os.path.join(ROOT, "fixtures", "data")
 
 

@@ -22,7 +22,7 @@ from conftest import fixture_paths
 
 pytestmark = pytest.mark.gpu
 
-CFGS = ["lines64", "lines1024", "grass4096", "hair512", "floorplan64"]
+CFGS = ["lines64", "lines1024", "grass4096", "hair512", "floorplan64", "grass4096l", "hair512r"]
 COHERENT = (9, 12)
 
 

@@ -66,7 +66,7 @@ def test_configs_on_device(cfg, which):
     if paths is None or f"{which}0_seg" not in g.files:
         pytest.skip("fixture/golden not generated")
     m = DeviceMesh.from_files(*paths)
-    box = (0.0, 0.0, 1.0, 0.5) if cfg == "grass4096" else (0.0, 0.0, 1.0, 1.0)
+    box = (0.0, 0.0, 1.0, 0.5) if cfg.startswith("grass") else (0.0, 0.0, 1.0, 1.0)
     for mode in (0, 1):
         if f"{which}{mode}_seg" not in g.files:
             continue
@@ -117,7 +117,7 @@ def test_degenerate_rays_on_device():
     k = 0
     while f"{k}_cfg" in g:
         cfg, index = str(g[f"{k}_cfg"]), int(g[f"{k}_index"])
-        box = (0.0, 0.0, 1.0, 0.5) if cfg == "grass4096" else (0.0, 0.0, 1.0, 1.0)
+        box = (0.0, 0.0, 1.0, 0.5) if cfg.startswith("grass") else (0.0, 0.0, 1.0, 1.0)
         ray = g[f"{k}_ray"]
         for w in ("cdt", "mwt"):
             m = DeviceMesh.from_files(*fixture_paths(cfg, w))

@@ -38,7 +38,7 @@ def timeit(fn, reps=20):
 
 
 for cfg in ("lines64", "lines1024", "grass4096", "hair512", "floorplan64"):
-    box = (0.0, 0.0, 1.0, 0.5) if cfg == "grass4096" else (0.0, 0.0, 1.0, 1.0)
+    box = (0.0, 0.0, 1.0, 0.5) if cfg.startswith("grass") else (0.0, 0.0, 1.0, 1.0)
     for which in ("mwt", "cdt"):
         d = os.path.join(ROOT, "fixtures", "data", cfg)
         mesh = DeviceMesh.from_files(os.path.join(d, "scene.txt"), os.path.join(d, f"{which}.tri"))

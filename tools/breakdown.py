@@ -13,7 +13,7 @@ from paper_2112_05570_b200.engine import DeviceMesh, new_histogram  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "lines1024"
 which = sys.argv[2] if len(sys.argv) > 2 else "cdt"
 n = 1 << 24
-box = (0.0, 0.0, 1.0, 0.5) if cfg == "grass4096" else (0.0, 0.0, 1.0, 1.0)
+box = (0.0, 0.0, 1.0, 0.5) if cfg.startswith("grass") else (0.0, 0.0, 1.0, 1.0)
 d = os.path.join(ROOT, "fixtures", "data", cfg)
 mesh = DeviceMesh.from_files(os.path.join(d, "scene.txt"), os.path.join(d, f"{which}.tri"))
 if len(sys.argv) > 4:

@@ -16,7 +16,7 @@ import bench  # noqa: E402
 if __name__ == "__main__":
     out = sys.argv[1] if len(sys.argv) > 1 else "like_for_like.json"
     res = {}
-    for cfg in ("lines1024", "grass4096", "hair512", "floorplan64"):
+    for cfg in ("lines1024", "grass4096", "hair512", "floorplan64", "grass4096l", "hair512r"):
         res[cfg] = bench.like_for_like(cfg, 0)
         r = res[cfg]
         print(cfg, {k: (round(v["rays_per_s"] / 1e9, 3), round(v["ops_per_ray"], 3))

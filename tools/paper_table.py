@@ -34,6 +34,8 @@ CONFIGS = {  # BASELINE.json configs: ray box and box-entry ray count
     "grass4096": ((0.0, 0.0, 1.0, 0.5), 1 << 24),
     "hair512": ((0.0, 0.0, 1.0, 1.0), 1 << 24),
     "floorplan64": ((0.0, 0.0, 1.0, 1.0), 1 << 26),
+    "grass4096l": ((0.0, 0.0, 1.0, 0.5), 1 << 24),
+    "hair512r": ((0.0, 0.0, 1.0, 1.0), 1 << 24),
     # Lines-1024's 2^22 "recursive" rays: origins uniform in the box (point-location path)
     "lines1024-interior": ((0.0, 0.0, 1.0, 1.0), 1 << 22),
 }

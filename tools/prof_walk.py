@@ -11,7 +11,7 @@ from paper_2112_05570_b200.engine import DeviceMesh  # noqa: E402
 
 cfg, which, mode, n = sys.argv[1], sys.argv[2], int(sys.argv[3]), int(sys.argv[4])
 refill, minb = int(sys.argv[5]), int(sys.argv[6])
-box = (0.0, 0.0, 1.0, 0.5) if cfg == "grass4096" else (0.0, 0.0, 1.0, 1.0)
+box = (0.0, 0.0, 1.0, 0.5) if cfg.startswith("grass") else (0.0, 0.0, 1.0, 1.0)
 d = os.path.join(ROOT, "fixtures", "data", cfg)
 mesh = DeviceMesh.from_files(os.path.join(d, "scene.txt"), os.path.join(d, f"{which}.tri"))
 _lib.check(_lib.lib.mwt_set_tuning(refill, minb, int(os.environ.get("MWT_VARIANT", "0"))))

@@ -14,7 +14,7 @@ from paper_2112_05570_b200.engine import DeviceMesh, new_histogram, summarize_hi
 cfg = sys.argv[1] if len(sys.argv) > 1 else "lines1024"
 which = sys.argv[2] if len(sys.argv) > 2 else "mwt"
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 1 << 24
-box = (0.0, 0.0, 1.0, 0.5) if cfg == "grass4096" else (0.0, 0.0, 1.0, 1.0)
+box = (0.0, 0.0, 1.0, 0.5) if cfg.startswith("grass") else (0.0, 0.0, 1.0, 1.0)
 d = os.path.join(ROOT, "fixtures", "data", cfg)
 if not os.path.exists(os.path.join(d, f"{which}.tri")):
     which = "cdt"

@@ -16,7 +16,7 @@ from paper_2112_05570_b200.engine import DeviceMesh, new_histogram  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "lines1024"
 d = os.path.join(ROOT, "fixtures", "data", cfg)
 mesh = DeviceMesh.from_files(os.path.join(d, "scene.txt"), os.path.join(d, "mwt.tri"))
-box = (0.0, 0.0, 1.0, 0.5) if cfg == "grass4096" else (0.0, 0.0, 1.0, 1.0)
+box = (0.0, 0.0, 1.0, 0.5) if cfg.startswith("grass") else (0.0, 0.0, 1.0, 1.0)
 n = 1 << 24
 hist = new_histogram()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
