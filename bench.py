@@ -213,10 +213,12 @@ def run_reference_arm(args, world: int, rank: int):
         v, cores, sample = cpu_reference(args, world, 0, budget_s=args.cpu_budget / max(1, args.steps))
         vals.append(v)
     v = float(np.mean(vals))
+    step_rays = sum(n for _, n in CONFIGS[args.config][1]) * (1 if args.scaling == "strong" else world)
     line = {
         "metric": "rays_per_s_mwt_walk", "value": v, "unit": "rays/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": None, "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
+        "ms_per_step": step_rays / v * 1e3,  # one step's rays at the sampled rate
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
         "dtype": "f64", "data": "synthetic (seeded rays, reference-built fixtures)",
         "config": config_dict(args, world),
         "cpu_baseline": {"value": v, "unit": "rays/s", "cores": cores, "kind": "port", "sample": sample,
