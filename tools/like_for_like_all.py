@@ -19,7 +19,8 @@ if __name__ == "__main__":
     for cfg in ("lines1024", "grass4096", "hair512", "floorplan64", "grass4096l", "hair512r"):
         res[cfg] = bench.like_for_like(cfg, 0)
         r = res[cfg]
-        print(cfg, {k: (round(v["rays_per_s"] / 1e9, 3), round(v["ops_per_ray"], 3))
-                    for k, v in r.items() if isinstance(v, dict)}, flush=True)
+        for order in ("coherent", "iid"):
+            print(cfg, order, {k: (round(v["rays_per_s"] / 1e9, 3), round(v["ops_per_ray"], 3))
+                               for k, v in r[order].items()}, flush=True)
     with open(out, "w") as fh:
         json.dump(res, fh, indent=1)
