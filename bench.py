@@ -176,6 +176,8 @@ def cpu_reference(args, world: int, rank: int, budget_s: float = 20.0):
     of the same workload (the first rays of every part, same generator order):
     returns (rays/s, cores, sample text)."""
     from oracle import oracle as orc
+    # every host thread this process may run on (torchrun sets OMP_NUM_THREADS=1 per rank)
+    orc.set_num_threads(len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count())
     box = CONFIGS[args.config][0]
     m = orc.Mesh.from_files(*fixture(args.config, args.mesh))
     cores = orc.num_threads()

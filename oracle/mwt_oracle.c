@@ -916,3 +916,13 @@ int orc_num_threads(void) {
     return 1;
 #endif
 }
+
+/* the thread count of later parallel regions (launchers such as torchrun set
+   OMP_NUM_THREADS=1 per rank; the CPU baseline uses every host thread) */
+void orc_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}

@@ -77,6 +77,7 @@ def lib():
         L.orc_kd_destroy.argtypes = [P]
         L.orc_kd_trace.argtypes = [P, P, P, i64, P, P, P, P, P, P, P]
         L.orc_num_threads.restype = ctypes.c_int
+        L.orc_set_num_threads.argtypes = [ctypes.c_int]
         _lib = L
     return _lib
 
@@ -284,3 +285,7 @@ class Kd:
 
 def num_threads() -> int:
     return lib().orc_num_threads()
+
+
+def set_num_threads(n: int) -> None:
+    lib().orc_set_num_threads(int(n))
