@@ -205,6 +205,75 @@ def cpu_reference(args, world: int, rank: int, budget_s: float = 20.0):
         " (oracle locate + walk, OpenMP over all host threads)"
 
 
+_PYREF = {}
+
+
+def _pyref_chunk(task):
+    """One chunk of rays through the unmodified reference (worker of
+    python_reference; the mesh was loaded before the fork)."""
+    lo, arr = task
+    from mintri.accel import TraversalError, traverse_triangulation
+    from mintri.geometry import Point, Ray
+    tri, index, loc = _PYREF["tri"], _PYREF["index"], _PYREF["loc"]
+    seg = np.full(len(arr), -1, np.int32)
+    steps = np.zeros(len(arr), np.int32)
+    for i, (ox, oy, dx, dy) in enumerate(arr.tolist()):
+        ray = Ray(Point(ox, oy), Point(dx, dy))
+        try:
+            hit, st = traverse_triangulation(tri, ray, loc.locate(ray.origin), index)
+        except TraversalError:
+            seg[i] = -2
+            continue
+        steps[i] = st.tri_steps
+        if hit is not None:
+            seg[i] = hit.seg
+    return lo, seg, steps
+
+
+def python_reference(args, budget_s: float = 8.0):
+    """The reference's own Python path (TriLocator.locate + traverse_triangulation
+    with a shared SceneIndex, accel.py:138-213, :284-289) from the unmodified
+    package in baseline/_ref, one forked worker per host core, on a bounded
+    sample of the workload's first rays; the results are checked against the
+    oracle on the same rays.  None when baseline/_ref is absent."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "mintri")):
+        return None
+    import multiprocessing as mp
+    sys.path.insert(0, ref)
+    from mintri.accel import SceneIndex, TriLocator
+    from mintri.scene import Scene
+    from mintri.trimesh import load_triangulation
+    from oracle import oracle as orc
+    scene_p, tri_p = fixture(args.config, args.mesh)
+    scene = Scene.load(scene_p)
+    tri = load_triangulation(tri_p, scene)
+    _PYREF.update(tri=tri, index=SceneIndex(scene), loc=TriLocator(tri))
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    base = CONFIGS[args.config][1][0][0]
+    box = CONFIGS[args.config][0]
+    probe = orc.raygen(mode_word(base, args.order), box, SEED, 0, 256)
+    t0 = time.perf_counter()
+    _pyref_chunk((0, probe))
+    per_ray = (time.perf_counter() - t0) / len(probe)
+    n = int(min(1 << 20, max(cores * 256, budget_s * cores / max(per_ray, 1e-9))))
+    n -= n % 256
+    arr = orc.raygen(mode_word(base, args.order), box, SEED, 0, n)
+    tasks = [(lo, arr[lo:lo + 256]) for lo in range(0, n, 256)]
+    with mp.get_context("fork").Pool(cores) as pool:
+        t0 = time.perf_counter()
+        res = pool.map(_pyref_chunk, tasks, chunksize=max(1, len(tasks) // (4 * cores)))
+        dt = time.perf_counter() - t0
+    seg = np.concatenate([r[1] for r in sorted(res, key=lambda r: r[0])])
+    steps = np.concatenate([r[2] for r in sorted(res, key=lambda r: r[0])])
+    o = orc.Mesh.from_files(scene_p, tri_p).trace(arr)
+    return {"value": n / dt, "unit": "rays/s", "cores": cores, "kind": "reference (Python, unmodified)",
+            "sample": f"{args.config}/{args.mesh} ({args.order} order): the first {n} "
+                      f"{part_name(base).replace('_', '-')} rays, multiprocessing pool (fork), one worker per core",
+            "matches_oracle": bool(np.array_equal(seg, o["seg"]) and np.array_equal(steps, o["steps"])),
+            "source": "baseline/_ref (tools/install_reference.sh)"}
+
+
 def run_reference_arm(args, world: int, rank: int):
     if rank != 0:
         return
@@ -227,6 +296,12 @@ def run_reference_arm(args, world: int, rank: int):
                          "cpu_model": cpu_model()},
         "e2e": {"value": v, "unit": "rays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    try:
+        pr = python_reference(args)
+    except Exception as e:  # noqa: BLE001
+        pr = {"error": f"{type(e).__name__}: {e}"}
+    if pr is not None:
+        line["cpu_baseline"]["python_reference"] = pr
     print(json.dumps(line), flush=True)
 
 
@@ -474,6 +549,12 @@ def main():
         v, cores, sample = cpu_reference(args, world, rank, budget_s=args.cpu_budget)
         line["cpu_baseline"] = {"value": v, "unit": "rays/s", "cores": cores, "kind": "port",
                                 "sample": sample, "cpu_model": cpu_model()}
+        try:  # the unmodified Python reference beside the port, when it was shipped
+            pr = python_reference(args)
+        except Exception as e:  # noqa: BLE001  (informational; never fails the bench)
+            pr = {"error": f"{type(e).__name__}: {e}"}
+        if pr is not None:
+            line["cpu_baseline"]["python_reference"] = pr
     if world > 1:
         dist.barrier()
     if rank == 0:
