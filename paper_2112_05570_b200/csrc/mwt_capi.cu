@@ -218,6 +218,7 @@ int mwt_mesh_create(const double *vx, const double *vy, int32_t nverts, const in
                          P.res > 0 ? 1.0 / P.res : 0.0};
     m->dev.nbsides = P.nbsides;
     m->dev.unit_sides = P.unit_sides;
+    m->dev.coord_small = P.coord_small;
     for (int k = 0; k < P.nbsides; k++) {
         const auto &S = P.sides[k];
         m->dev.bs[k] = mwt::MeshDev::BSide{S.axis, S.off, S.cnt, S.boff, S.nb, S.c, S.lo, S.hi, S.scale};

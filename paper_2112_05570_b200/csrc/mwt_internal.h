@@ -54,6 +54,7 @@ constexpr uint32_t kBExact = 0x80000000u;
 struct HostPacked {
     int32_t nv = 0, nt = 0, ns = 0;
     int32_t res = 0, anchors_not_strict = 0, flood_filter = 1;
+    int32_t coord_small = 1;  // every vertex coordinate finite and |.| <= 2^500 (see MeshDev)
     std::vector<int32_t> link;      // 4*nt
     std::vector<double> cxy;        // 6*nt
     std::vector<int32_t> step;      // 8*3*nt (32-B records)
@@ -151,6 +152,11 @@ struct MeshDev {
     const uint4 *ctri;
     int32_t tri_smem_bytes;  // 16 * nt + 16 * nv if that plus the blob fits kSmemWalkMax, else 0
     int32_t tri_seg_staged;  // ... and the segments fit after it
+    // every vertex coordinate is finite with |x|, |y| <= 2^500: for a ray
+    // with the same bound (|d| <= 2^500 too) the two products of side_of
+    // cannot overflow, and the walk loop decides the apex side by comparing
+    // them (k_trace's tight loop)
+    int32_t coord_small;
 };
 
 // K5 BVH (mwt_bvh_create).  A node visit reads both children's boxes and

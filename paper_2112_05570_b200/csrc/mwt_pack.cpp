@@ -375,6 +375,9 @@ int pack_mesh(const double *vx, const double *vy, int32_t nv, const int32_t *tv,
     P.flood_filter = 1;
     for (int k = 0; k < nv; k++)
         if (!(std::fabs(vx[k]) <= 4.0 && std::fabs(vy[k]) <= 4.0)) P.flood_filter = 0;
+    P.coord_small = 1;
+    for (int k = 0; k < nv; k++)
+        if (!(std::fabs(vx[k]) <= 0x1p500 && std::fabs(vy[k]) <= 0x1p500)) P.coord_small = 0;
     // seed grid: the reference's TriLocator uses max(2, int(sqrt(T/2))) cells
     // per side (accel.py:265-266); the device uses a 24x finer grid (~290 cells
     // per triangle; Lines-1024: 1080^2 cells, 4.7 MB, L2-resident) so the seed

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+#include <cmath>
 #include <cstdint>
 #include <mutex>
 
@@ -478,6 +479,10 @@ struct TraceOut {
 struct Launch {
     RaySrc src;
     TraceOut out;
+    // the tight loop may decide the apex side by comparing side_of's two
+    // products (see k_trace): the mesh is coord_small and, for generated rays,
+    // so is the box (loaded rays are checked per lane)
+    int cmp_side;
 };
 
 // Per-ray prologue result (raygen or load, locate, first triangle)
@@ -923,8 +928,17 @@ __global__ void __launch_bounds__(THREADS, MINB)
         // group only with steps < lim - kUnroll, so no step in it passes the guard;
         // the last few steps before the guard run in walk_step), and the stop
         // edge ends the lane's walk in the loop but its phase is set after it.
-        const int glim = lim - kUnroll;
+        // The apex side c = RN(p - q), p = RN(dx * RN(vy - oy)), q = RN(dy *
+        // RN(vx - ox)) (side_of, no contraction), is only compared with 0
+        // here, so the loop compares p with q: for finite p, q, RN(p - q) == 0
+        // iff p == q (gradual underflow) and it has the sign of p - q.  p and q
+        // are finite when the ray's and the mesh's coordinates are bounded by
+        // 2^500 (every lane of a bounded launch; a loaded ray outside the bound,
+        // or one with a NaN or infinity, takes walk_step's full rule instead).
+        const int glim = L.cmp_side ? lim - kUnroll : -1;
         bool fl = phase == 1 && s.fast && s.steps < glim;
+        if (!GEN)
+            fl = fl && fmax(fmax(fabs(r.ox), fabs(r.oy)), fmax(fabs(r.dx), fabs(r.dy))) <= 0x1p500;
         const bool entered = fl;
         // kn: the record of the triangle the lane enters next.  It stays a
         // valid record index throughout the loop (a lane that left keeps
@@ -940,10 +954,12 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     uint32_t wx, wy;
                     double2 A;
                     fetch_step<SMEM, TRI>(M, srec, stri, svxy, kn, wx, wy, A);
-                    const double c = side_of(r, A);
-                    const bool ok = fl && c != 0.0;
-                    const uint32_t nw = c > 0.0 ? wx : wy;  // E1 if c > 0, else E2
-                    s.steps += ok ? 1 : 0;
+                    const double p = r.dx * (A.y - r.oy), q = r.dy * (A.x - r.ox);  // c = p - q
+                    const bool ok = fl && p != q;
+                    const uint32_t nw = p > q ? wx : wy;  // E1 if c > 0, else E2
+                    // (a predicated add: the compiler's own form is an add and a select)
+                    asm("{.reg .pred q; setp.ne.b32 q, %1, 0; @q add.s32 %0, %0, 1;}"
+                        : "+r"(s.steps) : "r"((int)ok));
                     const bool go = ok && !(nw & (SMEM ? kCStop : kStopBit));
                     kn = go ? nw : kn;
                     fl = go;
@@ -1214,6 +1230,7 @@ int launch_trace(const MeshDev &m, const double *rays, const int32_t *start, int
         L.src.rays = rays + 4 * off;
         L.src.start = at(start);
         L.out = TraceOut{at(o_start), at(o_seg), at(o_steps), at(o_t), at(o_u), at(o_st), at(o_end)};
+        L.cmp_side = m.coord_small;
         launch_k_trace_any<false>(m, L, c, nullptr, stream);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return (int)e;
@@ -1227,6 +1244,9 @@ int launch_trace_generated(const MeshDev &m, int mode, const double *box, uint64
     if (n <= 0) return 0;
     RayGen g;
     if (!make_raygen(mode, box, seed, g)) return (int)cudaErrorInvalidValue;
+    // origins on or inside the box: |o| <= 2^500 when the box is (W * u <= 2^501)
+    bool box_small = true;
+    for (int k = 0; k < 4; k++) box_small = box_small && std::fabs(box[k]) <= 0x1p499;
     for (int64_t off = 0; off < n; off += kMaxLaunchRays) {  // see launch_trace
         const int64_t c = n - off < kMaxLaunchRays ? n - off : kMaxLaunchRays;
         auto at = [off](auto *p) { return p ? p + off : p; };
@@ -1234,6 +1254,7 @@ int launch_trace_generated(const MeshDev &m, int mode, const double *box, uint64
         L.src.gen = g;
         L.src.first = first + (uint64_t)off;
         L.out = TraceOut{nullptr, at(o_seg), at(o_steps), at(o_t), nullptr, nullptr, nullptr};
+        L.cmp_side = m.coord_small && box_small;  // generated directions have |d| <= 1
         launch_k_trace_any<true>(m, L, c, hist, stream);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return (int)e;
