@@ -69,3 +69,22 @@ def test_trace_host_entry_point(cfg):
     _compare(got, ref)
     got2 = mesh.trace(rays, ref["start"])  # explicit start triangles
     _compare(got2, ref)
+
+
+def test_unbounded_ray_takes_the_full_rule():
+    """The tight walk loop compares side_of's two products instead of
+    subtracting them (exact while |o|, |d| and the mesh stay within 2^500);
+    loaded rays outside that bound walk with the full rule.  Directions
+    scaled by 2^600 (exact) must give the oracle's results -- and the
+    unscaled rays' walk: every side value scales by the same power of two."""
+    from oracle import oracle as orc
+    mesh, om = _mesh_pair("floorplan64", "mwt")
+    rays = orc.raygen(0, box_of("floorplan64"), 3, 0, 4096)
+    big = rays.copy()
+    big[:, 2:] *= 2.0 ** 600
+    ref = om.trace(big)
+    got = mesh.trace(big)
+    _compare(got, ref)
+    base = mesh.trace(rays)
+    for k in ("start", "seg", "steps"):
+        assert np.array_equal(got[k], base[k]), k
