@@ -393,6 +393,12 @@ __device__ __forceinline__ bool walk_step(const MeshDev &M, const Ray &r, WalkSt
     return true;
 }
 
+#ifndef MWT_TERM_RCP
+#define MWT_TERM_RCP 0
+#endif
+// the hit test's two quotients: IEEE divisions (0) or one reciprocal (1)
+constexpr bool kTermRcp = MWT_TERM_RCP;
+
 // constrained / open exit: accel.py:192-211
 // (sseg: a shared-memory copy of the segments, or NULL)
 __device__ __forceinline__ int walk_terminal(const MeshDev &M, const Ray &r, const WalkState &s,
@@ -405,7 +411,7 @@ __device__ __forceinline__ int walk_terminal(const MeshDev &M, const Ray &r, con
     const double4 S = sseg ? sseg[sid] : ldg4d(M.seg + sid);
     double t, u;
     bool par = false;
-    bool ok = rsi<false>(r, S, t, u, par);
+    bool ok = rsi<kTermRcp>(r, S, t, u, par);
     if (par) st |= ST_PARALLEL;
     if (!ok) {
         // grazing numerical corner, accel.py:199-207
@@ -422,7 +428,7 @@ __device__ __forceinline__ int walk_terminal(const MeshDev &M, const Ray &r, con
         const double ex = S.z - S.x, ey = S.w - S.y;
         u = ((x - S.x) * ex + (y - S.y) * ey) / (ex * ex + ey * ey);  // Segment.param_of
     }
-    const int s2 = canonical<false>(M, r, sid, t, u, ot, ou);
+    const int s2 = canonical<kTermRcp>(M, r, sid, t, u, ot, ou);
     if (s2 != sid) st |= ST_CANON;
     return s2;
 }
@@ -723,16 +729,28 @@ __device__ __forceinline__ void fetch_step(const MeshDev &M, const uint2 *srec, 
 }
 
 #ifndef MWT_GRAB
-#define MWT_GRAB 128
+#define MWT_GRAB 512
+#endif
+#ifndef MWT_GRAB_TAIL
+#define MWT_GRAB_TAIL 128
 #endif
 #ifndef MWT_UNROLL
 #define MWT_UNROLL 5
 #endif
-constexpr int kGrab = MWT_GRAB;  // rays a warp takes from its CTA's counter at a time
+// Rays a warp takes from its CTA's counter at a time: kGrab (a whole
+// coherent group of the benchmark order, so a refill batch rarely spans two
+// groups or two grabs), kGrabTail once fewer than two big grabs per warp
+// are left in the CTA's range (the warps' last grabs stay short: balance).
+constexpr int kGrab = MWT_GRAB;
+constexpr int kGrabTail = MWT_GRAB_TAIL;
+#ifndef MWT_CTA_ALIGN
+#define MWT_CTA_ALIGN MWT_GRAB
+#endif
+constexpr long long kCtaAlign = MWT_CTA_ALIGN;
 constexpr int kUnroll = MWT_UNROLL;  // fast steps per warp vote
 
 // The trace kernel.  Each CTA owns a contiguous range of rays; its warps take
-// kGrab rays at a time from a shared counter (so all warps of a CTA finish
+// kGrab (kGrabTail) rays at a time from a shared counter (so all warps of a CTA finish
 // together), and each warp keeps its lanes busy: once at most `refill_below`
 // lanes are still walking, the lanes whose rays ended run the epilogue and
 // the idle lanes the prologue of the next rays, both as one batch.
@@ -832,7 +850,10 @@ __global__ void __launch_bounds__(THREADS, MINB)
         }
         bulk_stage(&stage_bar, np, dst, src, bytes);
     }
-    const long long per = (n + gridDim.x - 1) / gridDim.x;
+    // CTA ranges start at multiples of kGrab (MWT_CTA_ALIGN), so a big grab
+    // is one aligned block of ray indices -- one coherent group of the
+    // benchmark order -- rather than the tails of two
+    const long long per = ((n + gridDim.x - 1) / gridDim.x + kCtaAlign - 1) / kCtaAlign * kCtaAlign;
     const long long cbeg = (long long)blockIdx.x * per;
     const long long cend = cbeg + per < n ? cbeg + per : n;
     if (hist) {
@@ -883,11 +904,17 @@ __global__ void __launch_bounds__(THREADS, MINB)
                 unsigned nb = end, ne = end;
                 const int rem = (int)(end - next);
                 if (rem < nidle) {
-                    unsigned base = 0u;
-                    if (lane == 0) base = atomicAdd(&s_next, (unsigned)kGrab);
+                    unsigned base = 0u, g = (unsigned)kGrab;
+                    if (lane == 0) {
+                        const unsigned cur = *reinterpret_cast<volatile unsigned *>(&s_next);
+                        if (kGrabTail < kGrab && (cur >= span || span - cur < 2u * (THREADS / 32) * kGrab))
+                            g = (unsigned)kGrabTail;
+                        base = atomicAdd(&s_next, g);
+                    }
                     base = __shfl_sync(FULL, base, 0);
+                    g = __shfl_sync(FULL, g, 0);
                     nb = base < span ? base : span;
-                    ne = span - nb > (unsigned)kGrab ? nb + kGrab : span;
+                    ne = span - nb > g ? nb + g : span;
                 }
                 if (phase == 0) {
                     const unsigned o = rank < rem ? next + rank : nb + (rank - rem);
