@@ -82,7 +82,7 @@ def test_generated_kernel_equals_explicit_rays_and_histogram(cfg):
     from paper_2112_05570_b200.sharding import histogram_host
     paths = fixture_paths(cfg, "mwt") or fixture_paths(cfg, "cdt")
     m = DeviceMesh.from_files(*paths)
-    n = 1 << 18
+    n = (1 << 18) + 77  # (first = 777, n: neither a multiple of the 512-ray grabs nor of 128)
     from oracle import raygen as rg
     for mode in (0, 1, rg.coherent(0), rg.coherent(1)):
         h = new_histogram()
