@@ -358,21 +358,27 @@ def roofline(args, hb, kms, clocks, sms, local):
                                            "registers: 128 B per SM per cycle at the sampled SM clock "
                                            "(B300_MICROARCH.md smem/L1 crossbar)"}}
     cands = {}
-    if st is not None and st.get("rays") == hb["rays"]:
-        inst = st["warp_instructions"]
+    if st is not None and st.get("rays"):
+        # a capture of this launch size, or (a rank's shard of the headline
+        # workload) the same workload at another ray count: its counts per ray
+        scale = hb["rays"] / st["rays"]
+        inst = st["warp_instructions"] * scale
         ipk = sms * 4 * sm_mhz / 1e3
         cands["issue"] = {"achieved": inst / (kms / 1e3) / 1e9, "peak": ipk, "unit": "G warp-inst/s",
                           "note": "4 warp instructions per SM per cycle at the sampled SM clock"}
         wf = st.get("l1_wavefronts")
         if wf:
+            wf *= scale
             cands["l1_wavefront"] = {"achieved": wf / (kms / 1e3) / 1e9, "peak": sms * sm_mhz / 1e3,
                                      "unit": "G wavefronts/s",
                                      "note": "L1 data pipe (global + shared): one wavefront per SM per cycle"}
         for c in cands.values():
             c["frac"] = c["achieved"] / c["peak"]
         r["ncu_capture"] = {k: st.get(k) for k in ("file", "report", "build_id", "warp_instructions",
-                                                     "l1_wavefronts", "dram_bytes", "duration_ms")}
-        r["traffic"] = st.get("dram_bytes")
+                                                     "l1_wavefronts", "dram_bytes", "duration_ms", "rays")}
+        if scale != 1.0:
+            r["ncu_capture"]["scaled_to_rays"] = hb["rays"]
+        r["traffic"] = st.get("dram_bytes") * scale if st.get("dram_bytes") else None
     else:
         r["traffic"] = None
         r["ncu_capture"] = None
