@@ -100,3 +100,45 @@ def test_full_ray_set_matches_reference_digests(cfg, mesh):
         oerr = (ref["status"] & orc.ST_ERROR) != 0
         theirs = dg.chunk_digests(ref["seg"], ref["t"], ref["steps"], ref["start"], oerr, chunk)
         assert [tuple(x[:2]) for x in ref_chunks] == theirs, f"{cfg}/{mesh}: oracle != reference digests"
+
+
+@pytest.mark.parametrize("cfg,mesh", _cases())
+def test_full_iid_ray_set_matches_oracle(cfg, mesh):
+    """The iid generator order (no coherent groups) at the same BASELINE sizes:
+    every ray through the fused path and the explicit path, against the
+    oracle (pinned to the reference by the digests above and the goldens) on
+    the host's cores -- start, seg, steps, status and t bit-exact."""
+    import torch
+    from oracle import oracle as orc
+    from paper_2112_05570_b200.engine import DeviceMesh
+    D = dg.load(mesh)
+    if D is None or cfg not in D["configs"]:
+        pytest.skip(f"{cfg}/{mesh}: no BASELINE sizes recorded")
+    C = D["configs"][cfg]
+    box = tuple(C["box"])
+    paths = fixture_paths(cfg, mesh)
+    m = DeviceMesh.from_files(*paths)
+    om = orc.Mesh.from_files(*paths)
+    orc.set_num_threads(os.cpu_count() or 1)
+    step = 1 << 23
+    for part in C["parts"]:
+        base, n = part["mode"], part["n"]
+        for lo in range(0, n, step):
+            k = min(step, n - lo)
+            fused = m.trace_generated_device(base, box, 0, lo, k, outputs=True, hist=None)
+            rays = m.raygen_device(base, box, 0, lo, k)
+            ex = m.trace_device(rays, None, want=("start", "seg", "t", "steps", "status"))
+            torch.cuda.synchronize()
+            got = {x: v.cpu().numpy() for x, v in ex.items()}
+            for x in ("seg", "steps"):
+                assert np.array_equal(fused[x].cpu().numpy(), got[x]), f"{cfg}/{mesh}: fused != explicit ({x})"
+            del fused, rays, ex
+            ref = om.trace(orc.raygen(base, box, 0, lo, k))
+            st_bits = np.uint32(orc.ST_ERROR)
+            assert np.array_equal(got["status"].view(np.uint32) & st_bits, ref["status"] & st_bits)
+            ok = (ref["status"] & st_bits) == 0  # (the step count of a TraversalError is not a result)
+            for x in ("start", "seg", "steps"):
+                bad = np.nonzero((got[x] != ref[x]) & (ok if x == "steps" else True))[0]
+                assert len(bad) == 0, f"{cfg}/{mesh} rays {lo}+{bad[:5].tolist()}: {x} differs from the oracle"
+            hit = ref["seg"] >= 0
+            assert np.array_equal(got["t"][hit].view(np.uint64), ref["t"][hit].view(np.uint64))
