@@ -244,14 +244,24 @@ __device__ __forceinline__ void group_words(unsigned long long gs, unsigned long
     }
 }
 
-__device__ __forceinline__ Ray gen_ray(const RayGen &g, unsigned long long idx) {
+// gw (coherent order, may be NULL): a warp's cached group words {group's
+// stream, draw 0, draw 128} of one group (k_trace fills it per grab)
+__device__ __forceinline__ Ray gen_ray(const RayGen &g, unsigned long long idx,
+                                       const unsigned long long *gw = nullptr) {
     // per-ray SplitMix64 stream: draws mix64(s0 + (k + 1) * golden), s0 = key ^ index
     const unsigned long long s0 = g.key ^ idx;
     const unsigned long long gs = g.gkey ^ (idx >> g.gshift);  // the group's stream
     const Box &b = g.box;
     const unsigned m = __activemask();
     unsigned long long G0 = 0ull, G128 = 0ull;
-    if (g.cmask) group_words(gs, G0, G128);
+    if (g.cmask) {
+        if (gw && gw[0] == gs) {
+            G0 = gw[1];
+            G128 = gw[2];
+        } else {
+            group_words(gs, G0, G128);
+        }
+    }
     // unit-disk rejection: the first accepted attempt a in 0..63.  Later
     // attempts run while any lane of the warp still needs one, so the warp
     // stays converged (iid order: attempt 1 always -- nearly every warp needs

@@ -580,10 +580,10 @@ __device__ __forceinline__ int4 link_words(const MeshDev &M, const BTab &T, int 
 
 template <bool GEN>
 __device__ __forceinline__ Init prologue_body(const MeshDev &M, const BTab &T, const RaySrc &src,
-                                              long long i) {
+                                              long long i, const unsigned long long *gw = nullptr) {
     Init o;
     o.st = 0;
-    const Ray r = GEN ? gen_ray(src.gen, src.first + (unsigned long long)i)
+    const Ray r = GEN ? gen_ray(src.gen, src.first + (unsigned long long)i, gw)
                       : load_ray(src.rays, i);
     o.ox = r.ox; o.oy = r.oy; o.dx = r.dx; o.dy = r.dy;
     // (generated interior rays never start on the box: skip the table)
@@ -809,6 +809,7 @@ __global__ void __launch_bounds__(THREADS, MINB)
             long long *hist, int refill_below) {
     __shared__ HistSm<THREADS> H;
     __shared__ unsigned s_next;
+    __shared__ unsigned long long s_gw[GEN ? THREADS / 32 : 1][3];  // per warp: its grab's group words
     extern __shared__ __align__(16) unsigned char dsm[];
     const uint2 *srec = reinterpret_cast<const uint2 *>(dsm);
     const uint4 *stri = reinterpret_cast<const uint4 *>(dsm);
@@ -915,13 +916,28 @@ __global__ void __launch_bounds__(THREADS, MINB)
                     g = __shfl_sync(FULL, g, 0);
                     nb = base < span ? base : span;
                     ne = span - nb > g ? nb + g : span;
+                    if (GEN && L.src.gen.cmask && nb < ne) {
+                        // the group words of the grab's first ray, once per grab
+                        // (lane 0: draw 0, lane 1: draw 128); rays of another
+                        // group compute their own (gen_ray)
+                        const unsigned long long gs =
+                            L.src.gen.gkey ^ ((L.src.first + (unsigned long long)(cbeg + nb)) >> L.src.gen.gshift);
+                        const unsigned long long v = mix64(gs + (lane == 1 ? 129ull : 1ull) * kGolden);
+                        const unsigned long long v1 = __shfl_sync(FULL, v, 1);
+                        if (lane == 0) {
+                            s_gw[threadIdx.x >> 5][0] = gs;
+                            s_gw[threadIdx.x >> 5][1] = v;
+                            s_gw[threadIdx.x >> 5][2] = v1;
+                        }
+                        __syncwarp();
+                    }
                 }
                 if (phase == 0) {
                     const unsigned o = rank < rem ? next + rank : nb + (rank - rem);
                     if (rank < rem || o < ne) {
                         idx = o;
                         const long long i = cbeg + (long long)o;
-                        const Init in = prologue_body<GEN>(M, btab, L.src, i);
+                        const Init in = prologue_body<GEN>(M, btab, L.src, i, GEN ? s_gw[threadIdx.x >> 5] : nullptr);
                         if (!GEN && L.out.start) L.out.start[i] = in.start;
                         r.ox = in.ox; r.oy = in.oy; r.dx = in.dx; r.dy = in.dy;
                         s.w = in.w; s.kr = in.cur;
