@@ -468,6 +468,7 @@ __device__ __forceinline__ void hist_flush(unsigned int *h, unsigned long long s
 struct RaySrc {
     RayGen gen;        // generated rays (GEN == true)
     unsigned long long first;
+    int box_in4;       // the generator's box lies in [-4, 4]^2 (so does every origin)
     const double *rays;   // loaded rays (GEN == false)
     const int32_t *start; // optional given start triangles
 };
@@ -516,11 +517,12 @@ struct BTab {  // the boundary-edge table arrays (global or a shared-memory copy
     const double2 *svxy;
 };
 
+// box_in4: the origin is known to lie in [-4, 4]^2 (generated rays of a box inside it)
 __device__ __forceinline__ bool boundary_start(const MeshDev &M, const BTab &T, const Ray &r,
-                                               WalkState &s) {
+                                               WalkState &s, bool box_in4 = false) {
     // one validity flag instead of early returns (fewer divergent branches);
     // indices stay in range when a condition fails
-    bool ok = M.flood_filter && fabs(r.ox) <= 4.0 && fabs(r.oy) <= 4.0;
+    bool ok = M.flood_filter && (box_in4 || (fabs(r.ox) <= 4.0 && fabs(r.oy) <= 4.0));
     int k = -1;
     if (M.unit_sides) {  // bottom, right, top, left
         k = r.oy == 0.0 ? 0 : (r.ox == 1.0 ? 1 : (r.oy == 1.0 ? 2 : (r.ox == 0.0 ? 3 : -1)));
@@ -587,9 +589,9 @@ __device__ __forceinline__ Init prologue_body(const MeshDev &M, const BTab &T, c
                       : load_ray(src.rays, i);
     o.ox = r.ox; o.oy = r.oy; o.dx = r.dx; o.dy = r.dy;
     // (generated interior rays never start on the box: skip the table)
-    if (!src.start && !(GEN && src.gen.mode == MWT_RAYS_INTERIOR)) {
+    if ((GEN || !src.start) && !(GEN && src.gen.mode == MWT_RAYS_INTERIOR)) {  // (generated: no start ids)
         WalkState bs;
-        if (boundary_start(M, T, r, bs)) {
+        if (boundary_start(M, T, r, bs, GEN && src.box_in4)) {
             o.start = bs.kr / 3;
             o.w = bs.w; o.cur = bs.kr; o.ei = bs.ch; o.steps = 0;
             o.fast = true;
@@ -600,7 +602,7 @@ __device__ __forceinline__ Init prologue_body(const MeshDev &M, const BTab &T, c
     }
     double2 P0, P1, P2;
     int t0;
-    if (src.start) {
+    if (!GEN && src.start) {
         t0 = __ldg(src.start + i);
         if (t0 < 0 || t0 >= M.nt) t0 = -1;
         else corners(M, t0, P0, P1, P2);
@@ -687,9 +689,9 @@ __device__ __forceinline__ void epilogue(const MeshDev *__restrict__ Mg, const L
     const TraceOut &O = L->out;
     if (O.seg) O.seg[i] = seg;
     if (O.t) O.t[i] = t;
-    if (O.u) O.u[i] = u;
+    if (END && O.u) O.u[i] = u;  // (the generated-ray launch writes seg, t and steps only)
     if (O.steps) O.steps[i] = steps;
-    if (O.st) O.st[i] = st;
+    if (END && O.st) O.st[i] = st;
     if (END && O.end) O.end[i] = phase == 2 ? kr / 3 : -1;  // loaded rays only (chaining)
     if (H) hist_add_warp(H, seg, steps, st);
 }
@@ -1288,14 +1290,20 @@ int launch_trace_generated(const MeshDev &m, int mode, const double *box, uint64
     RayGen g;
     if (!make_raygen(mode, box, seed, g)) return (int)cudaErrorInvalidValue;
     // origins on or inside the box: |o| <= 2^500 when the box is (W * u <= 2^501)
-    bool box_small = true;
-    for (int k = 0; k < 4; k++) box_small = box_small && std::fabs(box[k]) <= 0x1p499;
+    bool box_small = true, box4 = true;
+    for (int k = 0; k < 4; k++) {
+        box_small = box_small && std::fabs(box[k]) <= 0x1p499;
+        // origins: box corners or x0 + RN(W u), u in [0, 1) -- within a few ulps
+        // of the box, so inside [-4, 4] for a box inside [-3.5, 3.5]
+        box4 = box4 && std::fabs(box[k]) <= 3.5;
+    }
     for (int64_t off = 0; off < n; off += kMaxLaunchRays) {  // see launch_trace
         const int64_t c = n - off < kMaxLaunchRays ? n - off : kMaxLaunchRays;
         auto at = [off](auto *p) { return p ? p + off : p; };
         Launch L{};
         L.src.gen = g;
         L.src.first = first + (uint64_t)off;
+        L.src.box_in4 = box4;
         L.out = TraceOut{nullptr, at(o_seg), at(o_steps), at(o_t), nullptr, nullptr, nullptr};
         L.cmp_side = m.coord_small && box_small;  // generated directions have |d| <= 1
         launch_k_trace_any<true>(m, L, c, hist, stream);
