@@ -24,7 +24,7 @@ def _mesh_pair(cfg, which):
     return DeviceMesh.from_files(*paths), orc.Mesh.from_files(*paths)
 
 
-def _compare(got, ref, keys=("start", "seg", "steps", "status")):
+def _compare(got, ref, keys=("start", "seg", "steps", "status"), t_bits=False):
     ok_err = (ref["status"] & 1) == 0
     for k in keys:
         a, b = np.asarray(got[k]), np.asarray(ref[k])
@@ -38,6 +38,9 @@ def _compare(got, ref, keys=("start", "seg", "steps", "status")):
         assert len(bad) == 0, f"{k}: {len(bad)} mismatches, first {bad[:5]} got {a[bad[:5]]} ref {b[bad[:5]]}"
     hit = ref["seg"] >= 0
     t_got, t_ref = got["t"][hit], ref["t"][hit]
+    if t_bits:  # (hit tests that overflow: inf / nan on both sides, bit for bit)
+        assert np.array_equal(t_got.view(np.uint64), t_ref.view(np.uint64))
+        return
     rel = np.abs(t_got - t_ref) / np.maximum(1.0, np.abs(t_ref))
     assert rel.max(initial=0.0) <= T_RTOL
     assert np.all(np.isnan(got["t"][~hit]))
@@ -88,3 +91,27 @@ def test_unbounded_ray_takes_the_full_rule():
     base = mesh.trace(rays)
     for k in ("start", "seg", "steps"):
         assert np.array_equal(got[k], base[k]), k
+
+
+def test_mesh_beyond_the_bound_walks_with_the_full_rule():
+    """A mesh whose coordinates exceed 2^500 (MeshDev.coord_small = 0) never
+    takes the compare-form tight loop: Lines-64 scaled by 2^600 (exact), its
+    box-entry rays' origins scaled alike, engine = oracle on every ray."""
+    import dataclasses
+    from oracle import oracle as orc
+    from paper_2112_05570_b200.engine import DeviceMesh
+    from paper_2112_05570_b200.formats import load_scene, load_tri
+    paths = fixture_paths("lines64", "mwt")
+    if paths is None:
+        pytest.skip("lines64/mwt fixture not generated")
+    K = 2.0 ** 600
+    sc, tr = load_scene(paths[0]), load_tri(paths[1])
+    mesh = DeviceMesh(dataclasses.replace(sc, xy=sc.xy * K), dataclasses.replace(tr, vxy=tr.vxy * K))
+    rs, rt = orc.load_scene(paths[0]), orc.load_tri(paths[1])
+    om = orc.Mesh(orc.RawScene(rs.ax * K, rs.ay * K, rs.bx * K, rs.by * K, rs.kind, rs.name),
+                  orc.RawTri(rt.vx * K, rt.vy * K, rt.v, rt.nbr, rt.flag))
+    rays = orc.raygen(0, (0.0, 0.0, 1.0, 1.0), 5, 0, 4096)
+    rays[:, :2] *= K
+    # (the hit test's products exceed the double range: t is inf or nan, as in
+    # the reference's Python floats -- compared bit for bit)
+    _compare(mesh.trace(rays), om.trace(rays), t_bits=True)
