@@ -524,7 +524,7 @@ def main():
                 f"{'annealed MWT' if args.mesh == 'mwt' else 'CDT'})",
         "config": config_dict(args, world),
         "workload_info": {"triangles": mesh.info.num_triangles, "segments": mesh.info.num_segments,
-                          "rays_per_rank": rays_per_rank, "parallelism": f"ray shards x{world}, mesh replicated",
+                          "rays_per_rank": rays_per_rank, "rays_per_s_per_gpu": value / world, "parallelism": f"ray shards x{world}, mesh replicated",
                           "l2": "flushed (256 MiB write) before every timed step",
                           "steps_per_ray": hsum["steps_per_ray"],
                           "hit_fraction": hsum["hits"] / max(1, hsum["rays"]),
